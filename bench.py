@@ -1,0 +1,360 @@
+"""Benchmark: enlarged-CG iterations/s on B200 (BASELINE.json metric), one JSON line.
+
+Default workload = BASELINE config 2 (SRE-CG2, t=16, full history, 3D Poisson
+64^3, box 4x2x2, b = A x*, x* ~ N(0,1) seed 1, tol 1e-8).  One "step" is one
+complete solve to tol (111 iterations); value = iterations / device time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--edge E]
+  python bench.py --impl reference ...   # the reference algorithm on the host CPU (oracle port)
+
+Under torchrun (N > 1) every rank runs an independent replica of the solve on
+its own GPU (row-sharded multi-GPU is not built yet -- DESIGN.md); timing is
+the max over ranks and value aggregates all ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "enlarged-CG iterations/s + HBM GB/s vs roofline at 1/2/4/8 B200"
+UNIT = "iterations/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--edge", type=int, default=None)
+    ap.add_argument("--form", default="stencil", choices=["stencil", "csr"])
+    ap.add_argument("--cpu-iters", type=int, default=None, help="iterations in the CPU baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")), \
+        int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons, sm, smax = set(), [], []
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                smax.append(float(r[1]))
+            except ValueError:
+                continue
+            for name, flag in zip(names, r[3:7]):
+                if flag.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (oracle port of the reference algorithm)
+# ---------------------------------------------------------------------------
+def cpu_sample(prob, iters):
+    from oracle import ekcg_oracle as orc
+    A = prob.csr()
+    kw = dict(prob.solver_kwargs)
+    t = kw.pop("t")
+    kw["kmax"] = iters
+    t0 = time.perf_counter()
+    out = orc.run_oracle(A.row_ptr, A.col_idx, A.values, prob.b, prob.partition.owner(), t, **kw)
+    dt = time.perf_counter() - t0
+    return out["iterations"], dt
+
+
+def cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def default_cpu_iters(config):
+    return {1: 130, 2: 12, 3: 2, 4: 1, 5: 1}.get(config, 5)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2305_19013_b200.problems import make_config
+    prob = make_config(args.config, args.edge, device_rhs=False)
+    iters = args.cpu_iters or default_cpu_iters(args.config)
+    for _ in range(max(0, min(args.warmup, 1))):
+        cpu_sample(prob, min(iters, 2))
+    tot_it, tot_s = 0, 0.0
+    for _ in range(args.steps):
+        it, dt = cpu_sample(prob, iters)
+        tot_it += it
+        tot_s += dt
+    value = tot_it / tot_s
+    sample = (f"first {iters} iterations of {prob.name} (reference algorithm, numpy/OpenBLAS oracle port), "
+              f"{args.steps} samples")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot_s / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": prob.name, "n": prob.n, "t": prob.solver_kwargs["t"],
+                   "iterations_per_step": iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores(), "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# GPU leg
+# ---------------------------------------------------------------------------
+class KernelTimer:
+    """CUDA-event timing of selected kernel launches on the launching stream."""
+
+    def __init__(self, torch, tags):
+        self.torch = torch
+        self.tags = set(tags)
+        self.events = {tag: [] for tag in tags}
+        self.enabled = False
+
+    def __call__(self, tag, fn):
+        if not self.enabled or tag not in self.tags:
+            fn()
+            return
+        e0 = self.torch.cuda.Event(enable_timing=True)
+        e1 = self.torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        self.events[tag].append((e0, e1))
+
+    def totals_ms(self):
+        return {tag: sum(a.elapsed_time(b) for a, b in ev) for tag, ev in self.events.items()}
+
+    def counts(self):
+        return {tag: len(ev) for tag, ev in self.events.items()}
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    import paper_2305_19013_b200 as pk
+    from paper_2305_19013_b200 import _lib
+    from paper_2305_19013_b200.engine import DeviceEngine
+    from paper_2305_19013_b200.problems import make_config
+
+    prob = make_config(args.config, args.edge)
+    cfg = pk.SolverConfig(**prob.solver_kwargs)
+    op = prob.stencil(dev) if args.form == "stencil" else pk.CsrOperator(prob.csr(), dev)
+    b_dev = torch.as_tensor(prob.b, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # 256 MB > L2 (126 MB)
+    timer = KernelTimer(torch, ["hist_gram", "hist_update", "spmm", "gram_self", "tri_apply"])
+
+    def solve_once(timed):
+        eng = DeviceEngine(op, prob.partition, cfg, device=dev)
+        eng.kernel_timer = timer
+        timer.enabled = timed
+        x, rep = eng.solve(b_dev)
+        return rep, eng
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    for _ in range(args.warmup):
+        solve_once(False)
+    barrier()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    launches0 = _lib.query("ekcg_launch_count")
+    step_ms, iters, reps, dgram = [], 0, [], []
+    for _ in range(args.steps):
+        flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        rep, eng = solve_once(True)
+        e1.record()
+        e1.synchronize()
+        step_ms.append(e0.elapsed_time(e1))
+        iters += rep.iterations
+        reps.append(rep)
+        dgram.extend(eng.launch_k)
+    barrier()
+    launches = _lib.query("ekcg_launch_count") - launches0
+    clk = clocks.stop()
+
+    tot_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        tot_ms = float(t.item())
+        it_t = torch.tensor([iters], device=dev, dtype=torch.float64)
+        dist.all_reduce(it_t)
+        iters_all = int(it_t.item())
+    else:
+        iters_all = iters
+    value = iters_all / (tot_ms / 1e3)
+
+    # ---- roofline of the dominant kernel (algorithmic bytes / event-timed duration) ----
+    n, m = prob.n, prob.solver_kwargs["t"] * prob.solver_kwargs.get("s", 1)
+    totals = timer.totals_ms()
+    counts = timer.counts()
+    bytes_alg = {"hist_gram": 0.0, "hist_update": 0.0}
+    for k, d, mm in dgram:
+        if d > 0:
+            bytes_alg["hist_gram"] += 2 * 8.0 * (d + 1) * n * mm      # two passes: read AQ_1..d and W
+            bytes_alg["hist_update"] += 2 * 8.0 * (d + 2) * n * mm    # two passes: read Q_1..d, W; write W
+    dom = max(("hist_gram", "hist_update"), key=lambda k: totals.get(k, 0.0))
+    hbm, peak_kind = peaks()
+    achieved = bytes_alg[dom] / (totals[dom] / 1e3) / 1e9 if totals.get(dom) else None
+    prof = ROOT / "profiles" / "r01_traffic.json"
+    traffic = None
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get(dom)
+    model_bytes = sum(r.model_bytes for r in reps)
+    model_time = model_bytes / (hbm * 1e9)
+    roofline = {
+        "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+        "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "kernel": dom,
+        "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
+        "kernel_ms_total": {k: round(v, 3) for k, v in totals.items()},
+        "kernel_launches": counts,
+        "step_model_gbs": model_bytes / (tot_ms / 1e3) / 1e9,
+        "step_model_frac": model_time / (tot_ms / 1e3),
+    }
+
+    # ---- e2e through the public API with host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        b_host = torch.from_numpy(np.ascontiguousarray(prob.b)).pin_memory()
+        e2e_ms, e2e_it = [], 0
+        for _ in range(max(1, args.steps)):
+            flush.fill_(1.0)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            x, rep = pk.enlarged_solve(op, b_host.numpy(), partition=prob.partition, cfg=cfg, device=dev)
+            e1.record()
+            e1.synchronize()
+            e2e_ms.append(e0.elapsed_time(e1))
+            e2e_it += rep.iterations
+        e2e_tot = sum(e2e_ms)
+        if world > 1:
+            t = torch.tensor([e2e_tot], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e2e_tot = float(t.item())
+            e2e_it *= world
+        e2e = {"value": e2e_it / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
+               "d2h_bytes_per_step": 8 * n + 8 * (reps[-1].iterations + 1)}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        it_cpu = args.cpu_iters or default_cpu_iters(args.config)
+        its, dt = cpu_sample(make_config(args.config, args.edge, device_rhs=False), it_cpu)
+        cpu = {"value": its / dt, "unit": UNIT, "cores": cores(), "kind": "port",
+               "sample": f"first {it_cpu} of {reps[-1].iterations} iterations of {prob.name} "
+                         f"(reference algorithm, numpy/OpenBLAS oracle port, {dt:.1f} s; early iterations "
+                         f"are the cheapest, so this overstates CPU speed)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": prob.name, "form": args.form, "n": n, "t": prob.solver_kwargs["t"],
+                       "s": prob.solver_kwargs.get("s", 1), "iterations_per_step": reps[-1].iterations,
+                       "status": reps[-1].status, "parallelism": "replicas" if world > 1 else "single",
+                       "l2": "flushed (256 MB write) before every timed step",
+                       "time_to_solution_ms": tot_ms / args.steps},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/* ekcg_b200.h -- C ABI of the B200 enlarged-CG hot-loop kernels.
+ *
+ * Every entry point is `extern "C"`, takes plain device pointers and sizes,
+ * never allocates, never synchronises, and launches on the CUDA stream passed
+ * as `void* stream` (a cudaStream_t; NULL = legacy default stream).  Return
+ * value: 0 = ok, -1 = invalid argument (nothing launched), -2 = launch error.
+ *
+ * Blocks are row-major n x m fp64 arrays with row stride `ld*` (>= m), the
+ * layout the reference's C-contiguous numpy blocks use, so each sparse row
+ * feeds m contiguous values.  `live` (may be NULL) is a device int: when it
+ * reads 0 the kernel returns immediately; the solver's finalize kernel clears
+ * it so iterations enqueued ahead of the host's status poll retire empty.
+ *
+ * The reference (`ekcg`, pure Python) has no FFI; each entry replaces the
+ * numpy/scipy call cited beside it (paths relative to pkg/src/ekcg/).  The
+ * Python driver binds these with ctypes (paper_2305_19013_b200/_lib.py);
+ * INTEGRATION.md shows the binding.
+ */
+#ifndef EKCG_B200_H
+#define EKCG_B200_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Grid stencil operator descriptor: the `_diffusion_matrix(shape, kappa)`
+ * operator (generators.py:25-60) with per-axis coefficients c* (1.0 = the
+ * reference) and node conductivity kappa(x,y,z) = kfield[(z/tz*fy + y/ty)*fx
+ * + x/tx] (kfield == NULL: kappa = kconst).  dim = 2 (nz ignored) or 3.
+ * Grid ordering is x-fastest (generators.py:9). */
+typedef struct EkcgStencil {
+    int dim;
+    int nx, ny, nz;
+    double cx, cy, cz;
+    const double* kfield;
+    int tx, ty, tz;
+    int fx, fy;
+    double kconst;
+} EkcgStencil;
+
+/* ---- sparse operator and T^t split ------------------------------------ */
+
+/* W[i, j] = (owner[i] == j) ? v[i] : +0.0 ; replaces Partition.split
+ * (partition.py:48-55).  Bit-exact. */
+int ekcg_split(const double* v, const int* owner, double* W, long long n, int t, int ldw,
+               const int* live, void* stream);
+
+/* W = split(v) + Wprev * diag(beta_sign * beta) ; the MSDO-CG candidate
+ * (solvers.py:378-382). */
+int ekcg_split_axpy(const double* v, const int* owner, const double* Wprev, int ldp,
+                    const double* beta, double beta_sign, double* W, long long n, int t, int ldw,
+                    const int* live, void* stream);
+
+/* Y = A X for CSR A (int64 row_ptr, int32 col_idx) ; replaces spmm/spmv
+ * (linalg.py:133-152).  Bit-exact with numpy's reduceat association. */
+int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const double* values,
+                  const double* X, int ldx, double* Y, int ldy, long long n, int m,
+                  const int* live, void* stream);
+
+/* Y = A X for the grid stencil operator; bit-exact with ekcg_spmm_csr on the
+ * CSR that generators.py:25-60 assembles for the same kappa. */
+int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
+                      int m, const int* live, void* stream);
+
+/* ---- tall-skinny block products (aortho.py:92-94,105,108; solvers.py:394-396) */
+
+/* Number of row chunks (split-K partials) ekcg_gram uses for these sizes. */
+int ekcg_gram_chunks(long long n, int d, int m1, int m2);
+
+/* partials[p][i][a][b] = sum over rows r of chunk p of X_i[r,a] * Y[r,b],
+ * for i < d.  Xs is a DEVICE array of d block pointers (row stride ldx,
+ * width m1); Y has width m2.  partials holds chunks * d * m1 * m2 doubles,
+ * chunks = ekcg_gram_chunks(n, d, m1, m2). Deterministic (no atomics). */
+int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2,
+              long long n, double* partials, const int* live, void* stream);
+
+/* out[j] = sum_{p < chunks} partials[p * len + j] in fixed order. */
+int ekcg_reduce(const double* partials, int chunks, long long len, double* out,
+                const int* live, void* stream);
+
+/* Wout = beta * Win + sign * sum_i Q_i C_i  (Q_i: n x m1 via device pointer
+ * array Qs; C: d*m1 x m2 row-major, block i at rows i*m1).  Wout may alias
+ * Win.  Replaces `W -= q_i @ C` (aortho.py:93-94) and, with d = 1, beta = 0,
+ * `trsm_right_inv` applied as W * R^{-1} (linalg.py:187-196). */
+int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1, const double* C,
+                      const double* Win, int ldwi, double* Wout, int ldwo, int m2,
+                      double beta, double sign, long long n, const int* live, void* stream);
+
+/* x += W alpha ; r -= AW alpha ; rho2_partials[p] = partial sum of r_new^2
+ * (solvers.py:394-397).  Uses ekcg_vec_chunks(n) partials. */
+int ekcg_vec_chunks(long long n);
+int ekcg_xr_update(const double* W, int ldw, const double* AW, int ldaw, const double* alpha, int m,
+                   double* x, double* r, long long n, double* rho2_partials,
+                   const int* live, void* stream);
+
+/* partials[p] = partial sum of v^2 (ekcg_vec_chunks(n) partials). */
+int ekcg_sumsq(const double* v, long long n, double* partials, const int* live, void* stream);
+
+/* dst[i, 0:w] = src[i, 0:w] for i < n (row strides lds, ldd): the s-step
+ * chain seed V1 = newest t columns of the cached A W (solvers.py:338-339). */
+int ekcg_copy_cols(const double* src, int lds, double* dst, int ldd, long long n, int w,
+                   const int* live, void* stream);
+
+/* out = a - b elementwise (r = b - A x, solvers.py:342). */
+int ekcg_sub(const double* a, const double* b, double* out, long long n, const int* live, void* stream);
+
+/* ---- small dense factorizations (linalg.py:164-184, aortho.py:74-79,98-110) */
+
+/* Pre-CholQR step: from Graw = W^T W (m x m), column norms D, G0 = sym(D^-1
+ * Graw D^-1), R0 = chol(G0); writes S0 = D^-1 R0^-1 (upper).  Breakdown
+ * (zero column or pivot <= tol * max diag) is recorded in ctrl and clears
+ * ctrl->live.  `ctrl` points at an EkcgCtrl block. */
+int ekcg_prechol(const double* Graw, int m, double* S0, void* ctrl, int iteration, double tol,
+                 void* stream);
+
+/* A-CholQR step: R = chol(sym(G)); writes S = R^-1 (upper). */
+int ekcg_cholinv(const double* G, int m, double* S, void* ctrl, int iteration, double tol,
+                 void* stream);
+
+/* Standalone Cholesky (no breakdown side effects): R (upper, m x m) and info
+ * = {0 ok | 1 breakdown, column, pivot-as-double-bits}. Test surface for
+ * cholesky_small (linalg.py:164-184). */
+int ekcg_cholesky(const double* B, int m, double tol, double* R, double* info, void* stream);
+
+/* ---- engine bookkeeping ------------------------------------------------ */
+
+/* Size in bytes of the control block. */
+int ekcg_ctrl_bytes(void);
+
+/* Initialise ctrl from rho0^2 = *rho2 : history[0] = rho0, tol_abs = tol*rho0,
+ * converged immediately when rho0 == 0. */
+int ekcg_start(void* ctrl, const double* rho2, double tol, double* history, void* stream);
+
+/* End of iteration k: rho = sqrt(*rho2), history[k] = rho, stagnation guard
+ * (window > 0), convergence (rho <= tol*rho0) and kmax checks (solvers.py:357,399,406-415). */
+int ekcg_finish(void* ctrl, const double* rho2, int k, int kmax, int stagnation_window,
+                double* history, void* stream);
+
+/* checks[slot] = sqrt(*rho2) when the solve is live (true residual log, solvers.py:401-402). */
+int ekcg_store_norm(const double* rho2, double* checks, int slot, const int* live, void* stream);
+
+/* Kernel launches issued through this library since load. */
+unsigned long long ekcg_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EKCG_B200_H */

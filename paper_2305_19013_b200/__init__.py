@@ -1,0 +1,69 @@
+"""B200-native hot loop of the memory-reduced enlarged CG family (arXiv 2305.19013).
+
+Drop-in for the reference `ekcg` solver path: same `enlarged_solve`,
+`SolverConfig`, `ConvergenceReport`, `SparseSpdMatrix`, `Partition` and
+per-kernel functions, executed by hand-written sm_100a fp64 kernels
+(libekcg_b200.so, C ABI in include/ekcg_b200.h).
+"""
+
+from .linalg import (
+    Breakdown,
+    SparseSpdMatrix,
+    cholesky_small,
+    gram,
+    norm2,
+    spmm,
+    spmv,
+    trsm_right_inv,
+)
+from .partition import Partition, contiguous_partition, read_partition, write_partition
+from .operators import CsrOperator, StencilOperator
+from .solvers import (
+    METHODS,
+    RETENTIONS,
+    BasisStore,
+    ConvergenceReport,
+    SolverConfig,
+    enlarged_solve,
+)
+from .problems import (
+    box_partition,
+    diffusion_csr,
+    gen_aniso3d,
+    gen_poisson2d,
+    gen_poisson3d,
+    gen_skyscraper,
+    make_config,
+)
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "Breakdown",
+    "SparseSpdMatrix",
+    "spmv",
+    "spmm",
+    "gram",
+    "cholesky_small",
+    "trsm_right_inv",
+    "norm2",
+    "Partition",
+    "contiguous_partition",
+    "read_partition",
+    "write_partition",
+    "CsrOperator",
+    "StencilOperator",
+    "METHODS",
+    "RETENTIONS",
+    "SolverConfig",
+    "ConvergenceReport",
+    "BasisStore",
+    "enlarged_solve",
+    "diffusion_csr",
+    "gen_poisson2d",
+    "gen_poisson3d",
+    "gen_aniso3d",
+    "gen_skyscraper",
+    "box_partition",
+    "make_config",
+]

@@ -1,0 +1,67 @@
+// Shared helpers for the ekcg B200 kernels (sm_100a, fp64).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define EKCG_OK 0
+#define EKCG_EINVAL -1
+#define EKCG_ELAUNCH -2
+
+// Global launch counter (read by bench.py through ekcg_launch_count()).
+extern unsigned long long g_ekcg_launches;
+
+// Every device-loop kernel takes an optional `live` flag.  The engine's
+// finalize kernel clears it when the solve stops (converged / maxiter /
+// breakdown), so iterations enqueued ahead of the host's status check
+// retire as empty launches.  nullptr means "always run".
+#define EKCG_GATE(live)                         \
+    do {                                        \
+        if ((live) != nullptr && *(live) == 0)  \
+            return;                             \
+    } while (0)
+
+static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static inline int launch_status() {
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? EKCG_OK : EKCG_ELAUNCH;
+}
+
+static inline unsigned grid_for(long long work, int block, long long cap = 148LL * 32) {
+    long long g = (work + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > cap) g = cap;
+    return (unsigned)g;
+}
+
+// IEEE round-to-nearest products/sums that nvcc may not contract into FMA.
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+
+// m8n8k4 fp64 tensor-core MMA (SASS: DMMA.8x8x4).  acc[0..1] += A(8x4) * B(4x8).
+// Fragment ownership (lane = threadIdx.x % 32):
+//   A: row lane>>2, col lane&3;   B: row (k) lane&3, col (n) lane>>2;
+//   C: row lane>>2, cols 2*(lane&3) + {0,1}.
+__device__ __forceinline__ void dmma_8x8x4(double (&acc)[2], double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(acc[0]), "+d"(acc[1])
+                 : "d"(a), "d"(b));
+}
+
+// Small control block shared by the device-side iteration loop.
+struct EkcgCtrl {
+    int live;          // 1 while the solve runs
+    int status;        // 0 running, 1 converged, 2 maxiter, 3 breakdown, 4 stagnated
+    int k_done;        // completed iterations (history length - 1)
+    int brk_kind;      // 0 none, 1 zero column, 2 pivot
+    int brk_col;
+    int brk_iter;
+    int best_k;
+    int pad;
+    double brk_pivot;
+    double brk_scale;
+    double rho0;
+    double tol_abs;    // tol * rho0
+    double best_rho;
+    double last_rho;
+};

@@ -1,0 +1,465 @@
+// Tall-skinny fp64 block kernels for the A-orthonormaliser and the iterate update.
+//
+//   ekcg_gram          C_i = X_i^T Y for a list of retained blocks (split-K partials)
+//   ekcg_reduce        fixed-order sum of the split-K partials (deterministic)
+//   ekcg_block_update  Wout = beta Win + sign sum_i Q_i C_i  (CGS2 update, W R^-1)
+//   ekcg_xr_update     x += W a, r -= AW a, partial |r|^2
+//
+// Block widths m in {8,16,32,64} run on the fp64 tensor cores (mma.sync
+// m8n8k4 -> SASS DMMA.8x8x4) with fragments loaded straight from the
+// row-major blocks: a fragment row is 4 consecutive doubles (32 B) of one
+// block row, so every DRAM sector fetched is consumed.  Other widths (the
+// reference's t = 1..7, mixed widths after a flexible switch) take the scalar
+// kernels.  No floating-point atomics anywhere: reruns are bit-identical.
+#include "common.cuh"
+#include "ekcg_b200.h"
+
+namespace {
+
+constexpr int kGramThreads = 128;  // 4 warps
+constexpr int kVecThreads = 256;
+
+// ---------------------------------------------------------------------------
+// chunking (split-K over rows)
+// ---------------------------------------------------------------------------
+long long rows_per_chunk(long long n, int chunks) {
+    long long r = (n + chunks - 1) / chunks;
+    return ((r + 15) / 16) * 16;
+}
+
+int gram_chunks(long long n, int d) {
+    const long long target = 148LL * 8;  // ~8 CTAs per SM in total
+    long long p = (target + d - 1) / d;
+    long long max_p = (n + 255) / 256;
+    if (p > max_p) p = max_p;
+    if (p < 1) p = 1;
+    return (int)p;
+}
+
+// ---------------------------------------------------------------------------
+// DMMA Gram: partials[p][i] (M x M) = X_i[rows of p]^T Y[rows of p]
+// Warp w: row lane ks = w % KS, output quadrant q = w / KS with TA x TB
+// tiles of 8x8.  Rows advance in k-steps of 4 (the mma K).
+// ---------------------------------------------------------------------------
+template <int M, int TA, int TB, int KS, int U>
+__global__ void __launch_bounds__(kGramThreads)
+gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, const double* __restrict__ Y, int ldy,
+                 long long n, long long rows_chunk, double* __restrict__ partials,
+                 const int* __restrict__ live) {
+    EKCG_GATE(live);
+    static_assert((M / 8 / TA) * (M / 8 / TB) * KS == kGramThreads / 32, "warp layout");
+    constexpr int QA = M / 8 / TA;
+    __shared__ double red[KS > 1 ? KS * M * M : 1];
+
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int ks = warp % KS;
+    const int quad = warp / KS;
+    const int a_base = (quad % QA) * TA * 8;
+    const int b_base = (quad / QA) * TB * 8;
+    const int i = blockIdx.y;
+    const double* __restrict__ X = Xs[i];
+    const long long r0 = blockIdx.x * rows_chunk;
+    long long r1 = r0 + rows_chunk;
+    if (r1 > n) r1 = n;
+    const long long steps = (r1 > r0) ? (r1 - r0 + 3) / 4 : 0;
+
+    double acc[TA][TB][2];
+#pragma unroll
+    for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+        for (int tb = 0; tb < TB; ++tb) acc[ta][tb][0] = acc[ta][tb][1] = 0.0;
+
+    const int lr = lane & 3;
+    const int lc = lane >> 2;
+    for (long long s0 = ks; s0 < steps; s0 += (long long)KS * U) {
+        double af[U][TA], bf[U][TB];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            long long s = s0 + (long long)u * KS;
+            long long r = r0 + 4 * s + lr;
+            bool ok = (s < steps) && (r < r1);
+            const double* xrow = X + r * ldx + a_base + lc;
+            const double* yrow = Y + r * ldy + b_base + lc;
+#pragma unroll
+            for (int ta = 0; ta < TA; ++ta) af[u][ta] = ok ? __ldg(xrow + 8 * ta) : 0.0;
+#pragma unroll
+            for (int tb = 0; tb < TB; ++tb) bf[u][tb] = ok ? __ldg(yrow + 8 * tb) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+                for (int tb = 0; tb < TB; ++tb) dmma_8x8x4(acc[ta][tb], af[u][ta], bf[u][tb]);
+    }
+
+    double* out = partials + ((long long)blockIdx.x * gridDim.y + i) * (M * M);
+    if (KS == 1) {
+#pragma unroll
+        for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+            for (int tb = 0; tb < TB; ++tb) {
+                int a = a_base + 8 * ta + lc;
+                int b = b_base + 8 * tb + 2 * lr;
+                out[a * M + b] = acc[ta][tb][0];
+                out[a * M + b + 1] = acc[ta][tb][1];
+            }
+    } else {
+#pragma unroll
+        for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+            for (int tb = 0; tb < TB; ++tb) {
+                int a = a_base + 8 * ta + lc;
+                int b = b_base + 8 * tb + 2 * lr;
+                red[(ks * M + a) * M + b] = acc[ta][tb][0];
+                red[(ks * M + a) * M + b + 1] = acc[ta][tb][1];
+            }
+        __syncthreads();
+        for (int o = threadIdx.x; o < M * M; o += kGramThreads) {
+            double s = red[o];
+#pragma unroll
+            for (int k = 1; k < KS; ++k) s += red[k * M * M + o];
+            out[o] = s;
+        }
+    }
+}
+
+// Scalar Gram for arbitrary (m1, m2): thread (row-group, output) pairs.
+__global__ void __launch_bounds__(256)
+gram_generic_kernel(const double* const* __restrict__ Xs, int ldx, int m1, const double* __restrict__ Y,
+                    int ldy, int m2, long long n, long long rows_chunk, double* __restrict__ partials,
+                    const int* __restrict__ live) {
+    EKCG_GATE(live);
+    extern __shared__ double sred[];
+    const int O = m1 * m2;
+    const int i = blockIdx.y;
+    const double* __restrict__ X = Xs[i];
+    const long long r0 = blockIdx.x * rows_chunk;
+    long long r1 = r0 + rows_chunk;
+    if (r1 > n) r1 = n;
+    double* out = partials + ((long long)blockIdx.x * gridDim.y + i) * O;
+    if (O <= 256) {
+        const int RG = 256 / O;
+        const int tid = threadIdx.x;
+        const int rg = tid / O;
+        const int o = tid % O;
+        double acc = 0.0;
+        if (rg < RG) {
+            const int a = o / m2, b = o % m2;
+            for (long long r = r0 + rg; r < r1; r += RG) acc += X[r * ldx + a] * Y[r * ldy + b];
+            sred[rg * O + o] = acc;
+        }
+        __syncthreads();
+        if (tid < O) {
+            double s = sred[o];
+            for (int k = 1; k < RG; ++k) s += sred[k * O + o];
+            out[o] = s;
+        }
+    } else {
+        for (int o = threadIdx.x; o < O; o += blockDim.x) {
+            const int a = o / m2, b = o % m2;
+            double acc = 0.0;
+            for (long long r = r0; r < r1; ++r) acc += X[r * ldx + a] * Y[r * ldy + b];
+            out[o] = acc;
+        }
+    }
+}
+
+__global__ void reduce_kernel(const double* __restrict__ partials, int chunks, long long len,
+                              double* __restrict__ out, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < len;
+         j += (long long)gridDim.x * blockDim.x) {
+        double s = partials[j];
+        for (int p = 1; p < chunks; ++p) s += partials[(long long)p * len + j];
+        out[j] = s;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// DMMA block update: Wout = beta Win + sign sum_i Q_i C_i   (m1 = m2 = M)
+// Warp tile: 8*MR rows x M columns; mma M-dim = rows, N = output column,
+// K = column of Q_i.
+// ---------------------------------------------------------------------------
+template <int M, int MR>
+__global__ void __launch_bounds__(128)
+update_dmma_kernel(const double* const* __restrict__ Qs, int ldq, int d, const double* __restrict__ C,
+                   const double* Win, int ldwi, double* Wout, int ldwo, double beta, double sign,
+                   long long n, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    constexpr int NT = M / 8;
+    constexpr int KK = M / 4;
+    const int lane = threadIdx.x & 31;
+    const int lr = lane & 3;
+    const int lc = lane >> 2;
+    const long long warps_total = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long tiles = (n + 8 * MR - 1) / (8 * MR);
+    for (long long tile = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); tile < tiles;
+         tile += warps_total) {
+        const long long rbase = tile * 8 * MR;
+        double acc[MR][NT][2];
+#pragma unroll
+        for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[mr][nt][0] = acc[mr][nt][1] = 0.0;
+
+        for (int i = 0; i < d; ++i) {
+            const double* __restrict__ Q = Qs[i];
+            const double* __restrict__ Ci = C + (long long)i * M * M;
+#pragma unroll
+            for (int kk = 0; kk < KK; ++kk) {
+                double bfr[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) bfr[nt] = __ldg(Ci + (4 * kk + lr) * M + 8 * nt + lc);
+                double afr[MR];
+#pragma unroll
+                for (int mr = 0; mr < MR; ++mr) {
+                    long long r = rbase + 8 * mr + lc;
+                    afr[mr] = (r < n) ? __ldg(Q + r * ldq + 4 * kk + lr) : 0.0;
+                }
+#pragma unroll
+                for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr], bfr[nt]);
+            }
+        }
+#pragma unroll
+        for (int mr = 0; mr < MR; ++mr) {
+            long long r = rbase + 8 * mr + lc;
+            if (r >= n) continue;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                int b = 8 * nt + 2 * lr;
+                double o0 = sign * acc[mr][nt][0];
+                double o1 = sign * acc[mr][nt][1];
+                if (beta != 0.0) {
+                    o0 = beta * Win[r * ldwi + b] + o0;
+                    o1 = beta * Win[r * ldwi + b + 1] + o1;
+                }
+                Wout[r * ldwo + b] = o0;
+                Wout[r * ldwo + b + 1] = o1;
+            }
+        }
+    }
+}
+
+__global__ void update_generic_kernel(const double* const* __restrict__ Qs, int ldq, int d, int m1,
+                                      const double* __restrict__ C, const double* Win, int ldwi,
+                                      double* Wout, int ldwo, int m2, double beta, double sign,
+                                      long long n, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    long long total = n * (long long)m2;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        long long r = e / m2;
+        int b = (int)(e - r * m2);
+        double s = 0.0;
+        for (int i = 0; i < d; ++i) {
+            const double* Q = Qs[i] + r * ldq;
+            const double* Ci = C + (long long)i * m1 * m2;
+            for (int a = 0; a < m1; ++a) s += Q[a] * Ci[a * m2 + b];
+        }
+        double o = sign * s;
+        if (beta != 0.0) o = beta * Win[r * ldwi + b] + o;
+        Wout[r * ldwo + b] = o;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// vector kernels with deterministic block partial sums
+// ---------------------------------------------------------------------------
+int vec_chunks(long long n) {
+    long long p = (n + kVecThreads - 1) / kVecThreads;
+    if (p > 148LL * 8) p = 148LL * 8;
+    if (p < 1) p = 1;
+    return (int)p;
+}
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double warp_sums[32];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (lane == 0) warp_sums[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        for (int w = 0; w < nw; ++w) s += warp_sums[w];
+    }
+    return s;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+xr_update_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ AW, int ldaw,
+                 const double* __restrict__ alpha, int m, double* __restrict__ x, double* __restrict__ r,
+                 long long n, double* __restrict__ partials, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    __shared__ double sa[256];
+    for (int a = threadIdx.x; a < m && a < 256; a += blockDim.x) sa[a] = alpha[a];
+    __syncthreads();
+    double sq = 0.0;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
+         row += (long long)gridDim.x * blockDim.x) {
+        const double* w = W + row * ldw;
+        const double* aw = AW + row * ldaw;
+        double dx = 0.0, dr = 0.0;
+        for (int a = 0; a < m; ++a) {
+            dx += w[a] * sa[a];
+            dr += aw[a] * sa[a];
+        }
+        x[row] = x[row] + dx;
+        double rn = r[row] - dr;
+        r[row] = rn;
+        sq += rn * rn;
+    }
+    double s = block_sum(sq);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kVecThreads)
+sumsq_kernel(const double* __restrict__ v, long long n, double* __restrict__ partials,
+             const int* __restrict__ live) {
+    EKCG_GATE(live);
+    double sq = 0.0;
+    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
+         row += (long long)gridDim.x * blockDim.x) {
+        double a = v[row];
+        sq += a * a;
+    }
+    double s = block_sum(sq);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+__global__ void copy_cols_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd,
+                                 long long n, int w, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    long long total = n * (long long)w;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        long long i = e / w;
+        int j = (int)(e - i * w);
+        dst[i * ldd + j] = src[i * lds + j];
+    }
+}
+
+__global__ void sub_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
+                           long long n, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x)
+        out[i] = a[i] - b[i];
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+extern "C" int ekcg_gram_chunks(long long n, int d, int m1, int m2) {
+    (void)m1;
+    (void)m2;
+    if (n < 1 || d < 1) return 1;
+    return gram_chunks(n, d);
+}
+
+extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2,
+                         long long n, double* partials, const int* live, void* stream) {
+    if (d < 1 || m1 < 1 || m2 < 1 || ldx < m1 || ldy < m2 || n < 1) return EKCG_EINVAL;
+    const int chunks = gram_chunks(n, d);
+    const long long rc = rows_per_chunk(n, chunks);
+    dim3 grid(chunks, d);
+    cudaStream_t st = as_stream(stream);
+    if (m1 == m2 && m1 == 8) {
+        gram_dmma_kernel<8, 1, 1, 4, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+    } else if (m1 == m2 && m1 == 16) {
+        gram_dmma_kernel<16, 2, 2, 4, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+    } else if (m1 == m2 && m1 == 32) {
+        gram_dmma_kernel<32, 4, 2, 2, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+    } else if (m1 == m2 && m1 == 64) {
+        gram_dmma_kernel<64, 4, 4, 1, 2><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+    } else {
+        const int O = m1 * m2;
+        size_t smem = (O <= 256) ? sizeof(double) * 256 : 0;
+        gram_generic_kernel<<<grid, 256, smem, st>>>(Xs, ldx, m1, Y, ldy, m2, n, rc, partials, live);
+    }
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_reduce(const double* partials, int chunks, long long len, double* out, const int* live,
+                           void* stream) {
+    if (chunks < 1 || len < 1) return EKCG_EINVAL;
+    reduce_kernel<<<grid_for(len, 256), 256, 0, as_stream(stream)>>>(partials, chunks, len, out, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1, const double* C,
+                                 const double* Win, int ldwi, double* Wout, int ldwo, int m2, double beta,
+                                 double sign, long long n, const int* live, void* stream) {
+    if (d < 1 || m1 < 1 || m2 < 1 || ldq < m1 || ldwo < m2 || n < 0) return EKCG_EINVAL;
+    if (beta != 0.0 && (Win == nullptr || ldwi < m2)) return EKCG_EINVAL;
+    if (n == 0) return EKCG_OK;
+    cudaStream_t st = as_stream(stream);
+    const bool even = (ldwo % 2 == 0) && (beta == 0.0 || ldwi % 2 == 0);
+    auto grid_rows = [&](int rows_per_warp) {
+        long long tiles = (n + rows_per_warp - 1) / rows_per_warp;
+        return grid_for(tiles, 4, 148LL * 16);
+    };
+    if (m1 == m2 && even && m1 == 8) {
+        update_dmma_kernel<8, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+                                                                  sign, n, live);
+    } else if (m1 == m2 && even && m1 == 16) {
+        update_dmma_kernel<16, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+                                                                   sign, n, live);
+    } else if (m1 == m2 && even && m1 == 32) {
+        update_dmma_kernel<32, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+                                                                   sign, n, live);
+    } else if (m1 == m2 && even && m1 == 64) {
+        update_dmma_kernel<64, 2><<<grid_rows(16), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+                                                                   sign, n, live);
+    } else {
+        update_generic_kernel<<<grid_for(n * m2, 256), 256, 0, st>>>(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo,
+                                                                     m2, beta, sign, n, live);
+    }
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_vec_chunks(long long n) { return vec_chunks(n); }
+
+extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ldaw, const double* alpha, int m,
+                              double* x, double* r, long long n, double* rho2_partials, const int* live,
+                              void* stream) {
+    if (m < 1 || m > 256 || ldw < m || ldaw < m || n < 1) return EKCG_EINVAL;
+    xr_update_kernel<<<vec_chunks(n), kVecThreads, 0, as_stream(stream)>>>(W, ldw, AW, ldaw, alpha, m, x, r, n,
+                                                                          rho2_partials, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_sumsq(const double* v, long long n, double* partials, const int* live, void* stream) {
+    if (n < 1) return EKCG_EINVAL;
+    sumsq_kernel<<<vec_chunks(n), kVecThreads, 0, as_stream(stream)>>>(v, n, partials, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_copy_cols(const double* src, int lds, double* dst, int ldd, long long n, int w,
+                              const int* live, void* stream) {
+    if (n < 0 || w < 1 || lds < w || ldd < w) return EKCG_EINVAL;
+    if (n == 0) return EKCG_OK;
+    copy_cols_kernel<<<grid_for(n * w, 256), 256, 0, as_stream(stream)>>>(src, lds, dst, ldd, n, w, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_sub(const double* a, const double* b, double* out, long long n, const int* live,
+                        void* stream) {
+    if (n < 1) return EKCG_EINVAL;
+    sub_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(a, b, out, n, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}

@@ -1,0 +1,510 @@
+"""Device engine: the `_run_engine` loop (solvers.py:319-428) as a stream of
+sm_100a kernel launches.
+
+One iteration (SRE-CG2, d retained blocks, width m = s*t) issues:
+
+  candidate   W = A W_{k-1} (cached, no copy) | split(r) | s-step chain | MSDO
+  CGS2 x 2    C = [AQ_1..AQ_d]^T W (DMMA split-K Gram) ; W <- W - sum Q_i C_i
+  Pre-CholQR  Graw = W^T W ; S0 = D^-1 chol(sym(D^-1 Graw D^-1))^-1 ; W0 = W S0
+  A-CholQR    G = W0^T (A W0) ; S = chol(sym G)^-1 ; W_k = W0 S ; AW_k = A W_k
+  update      alpha = W_k^T r ; x += W_k alpha ; r -= AW_k alpha ; rho = |r|
+  finish      history[k] = rho, stop test, stagnation guard (device)
+
+Every launch is gated on a device `live` flag that the Cholesky kernels
+(breakdown) and the finish kernel (converged / maxiter / stagnated) clear,
+so the host enqueues iterations ahead and polls the control block once per
+batch instead of synchronising every iteration.  The retained history is a
+ring of `trunc` slots in HBM (truncated / SRE-CG), or one block pair per
+iteration (full retention); the new block overwrites the oldest slot only
+after the second Gram-Schmidt pass has consumed it.
+"""
+
+from __future__ import annotations
+
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import get_device
+from .operators import as_operator
+from .solvers import BasisStore, ConvergenceReport
+
+_STATUS = {1: "converged", 2: "maxiter", 3: "breakdown", 4: "stagnated"}
+F64 = 8
+
+
+class _PtrArena:
+    """Write-once device arena of block-pointer arrays (the kernels take
+    `const double* const*`).  Each iteration pushes its pointer lists with one
+    async H2D copy from pinned memory; a region is rewritten only after a
+    stream sync."""
+
+    def __init__(self, device, capacity=1 << 15):
+        self.device = device
+        self.cap = capacity
+        self._alloc(capacity)
+
+    def _alloc(self, cap):
+        self.cap = cap
+        self.host = torch.empty(cap, dtype=torch.int64, pin_memory=True)
+        self.hnp = self.host.numpy()
+        self.dev = torch.empty(cap, dtype=torch.int64, device=self.device)
+        self.cur = 0
+
+    def push(self, ptrs):
+        L = len(ptrs)
+        if self.cur + L > self.cap:
+            torch.cuda.current_stream(self.device).synchronize()
+            if L > self.cap:
+                self._alloc(2 * L)
+            self.cur = 0
+        s = self.cur
+        self.hnp[s:s + L] = ptrs
+        self.dev[s:s + L].copy_(self.host[s:s + L], non_blocking=True)
+        self.cur += L
+        return self.dev.data_ptr() + F64 * s
+
+
+class _Block:
+    __slots__ = ("q", "aq", "width", "slot")
+
+    def __init__(self, q, aq, width, slot):
+        self.q, self.aq, self.width, self.slot = q, aq, width, slot
+
+
+class DeviceEngine:
+    """One solve of an enlarged-CG method on one GPU."""
+
+    def __init__(self, A, partition, cfg, device=None):
+        self.device = get_device(device)
+        self.op = as_operator(A, self.device)
+        self.n = int(self.op.n)
+        self.partition = partition
+        self.cfg = cfg
+        self.method = cfg.method
+        self.s = int(cfg.s)
+        self.retention = "trunc" if cfg.method == "sre-cg" else cfg.retention
+        self.window = cfg.effective_window()
+        self.kmax = cfg.kmax if cfg.kmax is not None else 2 * self.n
+        self.every = int(cfg.true_residual_every)
+        self.tol = float(cfg.tol)
+        self.stag_window = max(20, self.kmax // 10) if self.retention == "restart" else 0
+        self.sync_mode = False
+        self.max_lookahead = 16
+        self.kernel_timer = None  # optional hook: (name, callable) -> runs callable
+
+    # ------------------------------------------------------------------ setup
+    def _setup(self):
+        dev, n = self.device, self.n
+        self.stream = torch.cuda.current_stream(dev).cuda_stream
+        self.t_cur = int(self.partition.t)
+        self.m_max = self.s * self.t_cur
+        mm = self.m_max
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.WA = torch.empty(n * mm, **f64)
+        self.WB = torch.empty(n * mm, **f64)
+        self.WC = torch.empty(n * mm, **f64)
+        self.tmpv = torch.empty(n, **f64)
+        self.Graw = torch.empty(mm * mm, **f64)
+        self.G = torch.empty(mm * mm, **f64)
+        self.S0 = torch.empty(mm * mm, **f64)
+        self.S = torch.empty(mm * mm, **f64)
+        self.alpha = torch.empty(mm, **f64)
+        self.beta = torch.empty(mm, **f64)
+        self.rho2 = torch.empty(1, **f64)
+        self.tr2 = torch.empty(1, **f64)
+        self.vchunks = _lib.query("ekcg_vec_chunks", n)
+        self.vpart = torch.empty(self.vchunks, **f64)
+        self.part = torch.empty(1 << 16, **f64)
+        self.C = torch.empty(1 << 12, **f64)
+        self.ctrl = torch.zeros(_lib.query("ekcg_ctrl_bytes"), dtype=torch.uint8, device=dev)
+        self.ctrl_host = torch.empty(self.ctrl.numel(), dtype=torch.uint8, pin_memory=True)
+        self.live = self.ctrl.data_ptr()
+        self.history = torch.zeros(min(self.kmax, 4096) + 1, **f64)
+        self.checks = torch.zeros(max(1, min(self.kmax, 4096) // self.every + 1), **f64)
+        self.arena = _PtrArena(dev)
+        self.owner_dev = self.partition.device_owner(dev)
+        self.part_obj = self.partition
+        self.retained = []
+        self.slots = {}
+        self.since_clear = 0
+        self.cols = 0
+        self.peak = 0
+        self.restarts = []
+        self.switch_iteration = None
+        self.gram_chunks = {}
+        self.launch_k = []
+
+    def _ensure(self, name, numel):
+        buf = getattr(self, name)
+        if buf.numel() < numel:
+            buf = torch.empty(max(numel, 2 * buf.numel()), dtype=buf.dtype, device=self.device)
+            setattr(self, name, buf)
+        return buf
+
+    def _chunks(self, d):
+        c = self.gram_chunks.get(d)
+        if c is None:
+            c = _lib.query("ekcg_gram_chunks", self.n, d, 1, 1)
+            self.gram_chunks[d] = c
+        return c
+
+    # ---------------------------------------------------------- primitives
+    def _gram(self, xs_addr, ldx, d, m1, y_ptr, ldy, m2, out_ptr, tag="gram"):
+        """out (d*m1*m2) = [X_i^T Y] via split-K partials + fixed-order reduce."""
+        chunks = self._chunks(d)
+        part = self._ensure("part", chunks * d * m1 * m2)
+        run = lambda: _lib.call("ekcg_gram", xs_addr, ldx, d, m1, y_ptr, ldy, m2, self.n, part.data_ptr(),
+                                self.live, self.stream)
+        self._timed(tag, run)
+        _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m1 * m2, out_ptr, self.live, self.stream)
+
+    def _update(self, qs_addr, ldq, d, m1, c_ptr, win_ptr, ldwi, wout_ptr, ldwo, m2, beta, sign, tag="update"):
+        run = lambda: _lib.call("ekcg_block_update", qs_addr, ldq, d, m1, c_ptr, win_ptr, ldwi, wout_ptr, ldwo,
+                                m2, beta, sign, self.n, self.live, self.stream)
+        self._timed(tag, run)
+
+    def _apply_op(self, x_ptr, ldx, y_ptr, ldy, m, tag="spmm", live=-1):
+        gate = self.live if live == -1 else live
+        self._timed(tag, lambda: self.op.apply(x_ptr, ldx, y_ptr, ldy, m, gate, self.stream))
+
+    def _timed(self, tag, fn):
+        if self.kernel_timer is None:
+            fn()
+        else:
+            self.kernel_timer(tag, fn)
+
+    # -------------------------------------------------------------- store
+    def _new_block(self, width):
+        """Storage for W_k / AW_k.  Ring slot (trunc windows) or fresh pair (full)."""
+        n = self.n
+        if self.window is not None:
+            slot = self.since_clear % self.window
+            if slot not in self.slots:
+                f64 = dict(dtype=torch.float64, device=self.device)
+                self.slots[slot] = (torch.empty(n * self.m_max, **f64), torch.empty(n * self.m_max, **f64))
+            qbuf, aqbuf = self.slots[slot]
+        else:
+            slot = -1
+            f64 = dict(dtype=torch.float64, device=self.device)
+            qbuf, aqbuf = torch.empty(n * width, **f64), torch.empty(n * width, **f64)
+        return _Block(qbuf, aqbuf, width, slot)
+
+    def _append(self, blk):
+        self.retained.append(blk)
+        self.since_clear += 1
+        self.cols += blk.width
+        self.peak = max(self.peak, self.cols)
+        if self.window is not None:
+            while len(self.retained) > self.window:
+                old = self.retained.pop(0)
+                self.cols -= old.width
+
+    def _clear(self):
+        self.retained = []
+        self.since_clear = 0
+        self.cols = 0
+
+    # ------------------------------------------------------------ iteration
+    def _width_groups(self):
+        groups, start = [], 0
+        for i in range(1, len(self.retained) + 1):
+            if i == len(self.retained) or self.retained[i].width != self.retained[start].width:
+                groups.append((start, i, self.retained[start].width))
+                start = i
+        return groups
+
+    def _enqueue_iteration(self, k, tol1):
+        cfg, n = self.cfg, self.n
+        st, live = self.stream, self.live
+        # restart policies (solvers.py:358-364)
+        if k > 1 and self.retention == "restart" and k % cfg.restart_j == 1:
+            self._clear()
+            self.restarts.append(k)
+        elif (k > 1 and self.retention == "restart-tol" and tol1 < cfg.restart_tol
+              and (not self.restarts or k > self.restarts[-1] + 1)):
+            self._clear()
+            self.restarts.append(k)
+        switched = False
+        if (cfg.switch_tol is not None and self.switch_iteration is None and k > 1
+                and tol1 < cfg.switch_tol):
+            self.part_obj = self.part_obj.halve()
+            self.owner_dev = self.part_obj.device_owner(self.device)
+            self.t_cur //= 2
+            self.switch_iteration = k
+            switched = True
+
+        t = self.t_cur
+        m = self.s * t
+        d = len(self.retained)
+        groups = self._width_groups()
+        newest = self.retained[-1] if self.retained else None
+        blk = self._new_block(m)
+        WA, WB, WC = self.WA.data_ptr(), self.WB.data_ptr(), self.WC.data_ptr()
+        ptrs = [b.q.data_ptr() for b in self.retained] + [b.aq.data_ptr() for b in self.retained]
+        ptrs += [WA, WB, blk.q.data_ptr(), newest.aq.data_ptr() if newest is not None else 0]
+        base = self.arena.push(ptrs)
+        q_addr = lambda i: base + F64 * i
+        aq_addr = lambda i: base + F64 * (d + i)
+        WA_arr, WB_arr, NEW_arr, NEWEST_AQ_arr = (base + F64 * (2 * d + j) for j in range(4))
+
+        # ---- candidate block (solvers.py:366-382) ----
+        fresh = switched or not self.retained
+        W = WA
+        if fresh or self.method == "modified-msdo-cg":
+            _lib.call("ekcg_split", self.r.data_ptr(), self.owner_dev.data_ptr(), WA, n, t, m, live, st)
+            self._chain(WA, m, t)
+        elif self.method in ("sre-cg2", "sre-cg"):
+            if self.s == 1:
+                W = newest.aq.data_ptr()  # W_k = A W_{k-1}: read the cached product in place
+            else:
+                src = newest.aq.data_ptr() + F64 * (newest.width - t)
+                _lib.call("ekcg_copy_cols", src, newest.width, WA, m, n, t, live, st)
+                self._chain(WA, m, t)
+        else:  # msdo-cg: split(r) + W_prev diag(-(AW_prev^T r))
+            self._gram(NEWEST_AQ_arr, newest.width, 1, newest.width, self.r.data_ptr(), 1, 1,
+                       self.beta.data_ptr(), tag="gram_vec")
+            _lib.call("ekcg_split_axpy", self.r.data_ptr(), self.owner_dev.data_ptr(), newest.q.data_ptr(),
+                      newest.width, self.beta.data_ptr(), -1.0, WA, n, t, m, live, st)
+
+        # ---- CGS2 against the retained history (aortho.py:89-95) ----
+        if d > 0:
+            csz = sum((e - s0) * wg * m for s0, e, wg in groups)
+            C = self._ensure("C", csz)
+            for _ in range(2):
+                off = 0
+                for s0, e, wg in groups:  # all coefficients from the same W (classical GS)
+                    self._gram(aq_addr(s0), wg, e - s0, wg, W, m, m, C.data_ptr() + F64 * off, tag="hist_gram")
+                    off += (e - s0) * wg * m
+                off = 0
+                win = W
+                for s0, e, wg in groups:
+                    self._update(q_addr(s0), wg, e - s0, wg, C.data_ptr() + F64 * off, win, m, WA, m, m,
+                                 1.0, -1.0, tag="hist_update")
+                    win = WA
+                    off += (e - s0) * wg * m
+                W = WA
+
+        # ---- Pre-CholQR (aortho.py:98-110) ----
+        self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
+        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+        self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WB, m, m, 0.0, 1.0, tag="tri_apply")
+        self._apply_op(WB, m, WC, m, m)
+        self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_self")
+        _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+        self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
+                     tag="tri_apply")
+        self._apply_op(blk.q.data_ptr(), m, blk.aq.data_ptr(), m, m)
+        self._append(blk)
+
+        # ---- iterate update (solvers.py:394-399) ----
+        self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
+        self._timed("xr_update", lambda: _lib.call(
+            "ekcg_xr_update", blk.q.data_ptr(), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
+            self.x.data_ptr(), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st))
+        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
+        if k % self.every == 0:  # true-residual drift log (solvers.py:401-402)
+            slot = k // self.every - 1
+            self._ensure_checks(slot + 1)
+            self._residual_sq(self.x, self.tr2, live)
+            _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
+        self._ensure_history(k + 1)
+        _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+                  self.history.data_ptr(), st)
+        self._account(k, d, m, fresh, t)
+
+    def _chain(self, V, m, t):
+        """s-step chain V^(i+1) = A V^(i) on column slabs of width t (s-step)."""
+        for i in range(1, self.s):
+            self._apply_op(V + F64 * (i - 1) * t, m, V + F64 * i * t, m, t, tag="spmm_chain")
+
+    def _residual_sq(self, x, out, live):
+        """out = |b - A x|^2 (solvers.py:342,401)."""
+        self._apply_op(x.data_ptr(), 1, self.tmpv.data_ptr(), 1, 1, tag="spmv", live=live)
+        _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), self.tmpv.data_ptr(), self.n, live,
+                  self.stream)
+        _lib.call("ekcg_sumsq", self.tmpv.data_ptr(), self.n, self.vpart.data_ptr(), live, self.stream)
+        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, out.data_ptr(), live, self.stream)
+
+    def _ensure_history(self, length):
+        if self.history.numel() < length:
+            new = torch.zeros(max(length, 2 * self.history.numel()), dtype=torch.float64, device=self.device)
+            new[: self.history.numel()].copy_(self.history)
+            self.history = new
+
+    def _ensure_checks(self, length):
+        if self.checks.numel() < length:
+            new = torch.zeros(max(length, 2 * self.checks.numel()), dtype=torch.float64, device=self.device)
+            new[: self.checks.numel()].copy_(self.checks)
+            self.checks = new
+
+    def _account(self, k, d, m, fresh, t):
+        """Record (k, d, m) for the traffic/flop model and peak replay."""
+        self.launch_k.append((k, d, m))
+
+    def _nnz(self):
+        if hasattr(self.op, "nnz"):
+            return self.op.nnz
+        shape = self.op.shape
+        tot = self.n
+        for ax in range(len(shape)):
+            other = self.n // shape[ax]
+            tot += 2 * (shape[ax] - 1) * other
+        return tot
+
+    # -------------------------------------------------------------- control
+    def _read_ctrl(self):
+        self.ctrl_host.copy_(self.ctrl, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        raw = self.ctrl_host.numpy()
+        ints = raw[:32].view(np.int32)
+        dbl = raw[32:80].view(np.float64)
+        return {
+            "live": int(ints[0]), "status": int(ints[1]), "k_done": int(ints[2]), "brk_kind": int(ints[3]),
+            "brk_col": int(ints[4]), "brk_iter": int(ints[5]), "brk_pivot": float(dbl[0]),
+            "brk_scale": float(dbl[1]), "rho0": float(dbl[2]), "tol_abs": float(dbl[3]),
+            "last_rho": float(dbl[5]),
+        }
+
+    # ---------------------------------------------------------------- solve
+    def solve(self, b, x0=None, x_star=None, on_iteration=None):
+        cfg = self.cfg
+        dev = self.device
+        numpy_io = not isinstance(b, torch.Tensor)
+        self._setup()
+        t_wall0 = time.perf_counter()
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record()
+        self.b = torch.as_tensor(b, dtype=torch.float64).to(dev, non_blocking=False).contiguous()
+        if x0 is None:
+            self.x = torch.zeros(self.n, dtype=torch.float64, device=dev)
+        else:
+            self.x = torch.as_tensor(x0, dtype=torch.float64).to(dev).clone().contiguous()
+        self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
+        st = self.stream
+        # r = b - A x ; rho0 = |r|  (solvers.py:341-343)
+        self._apply_op(self.x.data_ptr(), 1, self.tmpv.data_ptr(), 1, 1, tag="spmv", live=None)
+        _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), self.r.data_ptr(), self.n, None, st)
+        _lib.call("ekcg_sumsq", self.r.data_ptr(), self.n, self.vpart.data_ptr(), None, st)
+        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), None, st)
+        _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
+
+        sync_each = (on_iteration is not None or self.retention == "restart-tol"
+                     or cfg.switch_tol is not None or self.sync_mode)
+        host_hist = None
+        if sync_each:
+            c = self._read_ctrl()
+            host_hist = [c["rho0"]]
+        k = 1
+        lookahead = 1
+        tol1 = 1.0
+        ctrl = None
+        while k <= self.kmax:
+            if sync_each:
+                self._enqueue_iteration(k, tol1)
+                ctrl = self._read_ctrl()
+                if ctrl["k_done"] == k:
+                    rho = ctrl["last_rho"]
+                    tol1 = abs(rho - host_hist[-1]) / host_hist[0]
+                    host_hist.append(rho)
+                    if on_iteration is not None:
+                        on_iteration(self._state(k, rho, tol1, numpy_io))
+                if ctrl["live"] == 0:
+                    break
+                k += 1
+            else:
+                for _ in range(lookahead):
+                    if k > self.kmax:
+                        break
+                    self._enqueue_iteration(k, 1.0)
+                    k += 1
+                ctrl = self._read_ctrl()
+                if ctrl["live"] == 0:
+                    break
+                lookahead = min(2 * lookahead, self.max_lookahead)
+        if ctrl is None:
+            ctrl = self._read_ctrl()
+        ev1.record()
+        ev1.synchronize()
+        solve_s = ev0.elapsed_time(ev1) / 1e3
+        return self._report(ctrl, x_star, numpy_io, solve_s, time.perf_counter() - t_wall0)
+
+    def _state(self, k, rho, tol1, numpy_io):
+        conv = (lambda t: t.cpu().numpy()) if numpy_io else (lambda t: t.clone())
+        blocks = [(b.q[: self.n * b.width].view(self.n, b.width), b.aq[: self.n * b.width].view(self.n, b.width))
+                  for b in self.retained]
+        return {"k": k, "x": conv(self.x), "r": conv(self.r), "rho": rho, "tol1": tol1,
+                "store": BasisStore(self.window, blocks, self.peak, to_host=numpy_io),
+                "partition": self.part_obj}
+
+    def _report(self, ctrl, x_star, numpy_io, solve_s, wall_s):
+        status_code = ctrl["status"]
+        k_done = ctrl["k_done"]
+        status = _STATUS.get(status_code)
+        if status is None:
+            # loop exhausted kmax without the device flag (cannot happen) or rho0 == 0
+            status = "converged" if ctrl["last_rho"] <= ctrl["tol_abs"] else "maxiter"
+        notes = []
+        if status_code == 3:
+            if ctrl["brk_kind"] == 1:
+                msg = f"zero column {ctrl['brk_col']} entering Pre-CholQR"
+            else:
+                msg = f"pivot {ctrl['brk_pivot']:.3e} at column {ctrl['brk_col']} (scale {ctrl['brk_scale']:.3e})"
+            notes.append(f"basis breakdown at iteration {ctrl['brk_iter']}: {msg}")
+        elif status_code == 4:
+            notes.append(f"no residual decrease over {self.stag_window} iterations")
+        history = self.history[: k_done + 1].cpu().numpy().copy()
+        last_attempted = k_done + 1 if status_code == 3 else k_done
+        # host bookkeeping ran ahead: replay the store model up to the real stop
+        restarts = [r for r in self.restarts if r <= last_attempted]
+        switch_it = self.switch_iteration if (self.switch_iteration or 0) <= last_attempted else None
+        peak = self._replay_peak(k_done)
+        nchecks = k_done // self.every
+        checks_v = self.checks[:nchecks].cpu().numpy() if nchecks else np.zeros(0)
+        checks = [((i + 1) * self.every, float(checks_v[i])) for i in range(nchecks)]
+        # true residual and relative error (solvers.py:289-291)
+        self._residual_sq(self.x, self.tr2, None)
+        true_res = float(torch.sqrt(self.tr2).item())
+        rel = None
+        if x_star is not None:
+            xs = torch.as_tensor(x_star, dtype=torch.float64).to(self.device)
+            rel = float((torch.linalg.vector_norm(self.x - xs) / torch.linalg.vector_norm(xs)).item())
+        x_out = self.x.cpu().numpy() if numpy_io else self.x
+        model_bytes = sum(self._iter_bytes(d, m) for kk, d, m in self.launch_k if kk <= k_done)
+        model_flops = sum(self._iter_flops(d, m) for kk, d, m in self.launch_k if kk <= k_done)
+        rep = ConvergenceReport(
+            status=status, iterations=len(history) - 1, residual_history=history,
+            switch_iteration=switch_it, restart_iterations=restarts, peak_block_vectors=peak,
+            relative_error=rel, true_residual=true_res, true_residual_checks=checks, x=x_out, notes=notes,
+            solve_seconds=solve_s, iterations_per_second=(k_done / solve_s if solve_s > 0 else None),
+            model_bytes=model_bytes, model_flops=model_flops)
+        rep.wall_seconds = wall_s
+        return x_out, rep
+
+    def _iter_bytes(self, d, m):
+        n = self.n
+        return 8.0 * ((4 * d + 11) * n * m + 5 * n) + 2 * self.op.matrix_bytes()
+
+    def _iter_flops(self, d, m):
+        n = self.n
+        return (8 * d + 6) * m * m * n + 4.0 * self._nnz() * m + 6.0 * m * n
+
+    def _replay_peak(self, k_done):
+        """peak_block_vectors with append-before-trim (solvers.py:163-170) over completed iterations."""
+        cols, peak, blocks = 0, 0, []
+        restarts = set(self.restarts)
+        for kk, d, m in self.launch_k:
+            if kk > k_done:
+                break
+            if kk in restarts:
+                blocks, cols = [], 0
+            blocks.append(m)
+            cols += m
+            peak = max(peak, cols)
+            if self.window is not None:
+                while len(blocks) > self.window:
+                    cols -= blocks.pop(0)
+        return peak

@@ -1,0 +1,140 @@
+"""Device operators A: CSR SpMM and the structured-grid stencil (the `op` seam of
+`_run_engine`, solvers.py:285-286,319).
+
+Both apply Y = A X to row-major blocks with arbitrary row strides, so the
+s-step chain can multiply column slabs of one n x (s*t) block in place.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import current_stream_ptr, get_device
+
+
+def _ptr(x):
+    return x if isinstance(x, int) else x.data_ptr()
+
+
+class CsrOperator:
+    """General SPD matrix in CSR; bit-exact with the reference spmm/spmv."""
+
+    kind = "csr"
+
+    def __init__(self, A, device=None):
+        self.device = get_device(device)
+        self.n = int(A.n)
+        if hasattr(A, "device_arrays"):
+            self.row_ptr, self.col_idx, self.values = A.device_arrays(self.device)
+        else:  # duck-typed reference matrix (ekcg.SparseSpdMatrix)
+            self.row_ptr = torch.from_numpy(np.ascontiguousarray(A.row_ptr, dtype=np.int64)).to(self.device)
+            self.col_idx = torch.from_numpy(np.ascontiguousarray(A.col_idx, dtype=np.int32)).to(self.device)
+            self.values = torch.from_numpy(np.ascontiguousarray(A.values, dtype=np.float64)).to(self.device)
+        self.nnz = int(self.col_idx.numel())
+        self.host = A
+
+    def matrix_bytes(self):
+        """Bytes of A streamed per application (int64 row_ptr, int32 col, f64 val)."""
+        return 8 * (self.n + 1) + 12 * self.nnz
+
+    def apply(self, X, ldx, Y, ldy, m, live=None, stream=None):
+        st = current_stream_ptr(self.device) if stream is None else stream
+        _lib.call("ekcg_spmm_csr", self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.values.data_ptr(),
+                  _ptr(X), ldx, _ptr(Y), ldy, self.n, m, live, st)
+
+
+class StencilOperator:
+    """`_diffusion_matrix(shape, kappa)` (generators.py:25-60) applied matrix-free.
+
+    shape: (nx, ny) or (nx, ny, nz), x fastest.
+    kappa: None / scalar (constant), or a tile field `field` of shape
+           (fz, fy, fx) / (fy, fx) with tile edge `tile` = (tx, ty[, tz]);
+           tile (1,1,1) with a full-size field is a node-by-node kappa.
+    axis_coef: per-axis multipliers (cx, cy[, cz]) on face and boundary
+           coefficients; all ones reproduces the reference generator exactly.
+    """
+
+    kind = "stencil"
+
+    def __init__(self, shape, kappa=None, tile=None, axis_coef=None, device=None):
+        self.device = get_device(device)
+        shape = tuple(int(s) for s in shape)
+        if len(shape) not in (2, 3) or min(shape) < 2:
+            raise ValueError(f"grid dimensions must be >= 2, got {shape}")
+        self.shape = shape
+        self.dim = len(shape)
+        self.n = int(np.prod(shape))
+        coef = tuple(float(c) for c in (axis_coef or (1.0,) * self.dim))
+        if len(coef) != self.dim:
+            raise ValueError("axis_coef needs one entry per grid axis")
+        self.axis_coef = coef
+        desc = _lib.EkcgStencil()
+        desc.dim = self.dim
+        desc.nx, desc.ny = shape[0], shape[1]
+        desc.nz = shape[2] if self.dim == 3 else 1
+        desc.cx, desc.cy = coef[0], coef[1]
+        desc.cz = coef[2] if self.dim == 3 else 1.0
+        self.field = None
+        if kappa is None or np.isscalar(kappa):
+            desc.kfield = None
+            desc.kconst = 1.0 if kappa is None else float(kappa)
+            desc.tx = desc.ty = desc.tz = 1
+            desc.fx = desc.fy = 1
+            self.field_host = None
+        else:
+            field = np.ascontiguousarray(np.asarray(kappa, dtype=np.float64))
+            tile = tuple(int(v) for v in (tile or (1,) * self.dim))
+            if len(tile) != self.dim:
+                raise ValueError("tile needs one entry per grid axis")
+            need = tuple(-(-s // t) for s, t in zip(shape, tile))  # tiles per axis (x, y[, z])
+            if field.shape != need[::-1]:
+                if field.size == self.n and all(t == 1 for t in tile):
+                    field = field.reshape(shape[::-1])
+                else:
+                    raise ValueError(f"kappa field shape {field.shape} != tiles {need[::-1]}")
+            if not np.all(np.isfinite(field)) or np.any(field <= 0.0):
+                raise ValueError("kappa must be finite and positive")
+            self.field_host = field
+            self.field = torch.from_numpy(field.reshape(-1)).to(self.device)
+            desc.kfield = self.field.data_ptr()
+            desc.tx, desc.ty = tile[0], tile[1]
+            desc.tz = tile[2] if self.dim == 3 else 1
+            desc.fx, desc.fy = need[0], need[1]
+            desc.kconst = 0.0
+        self.tile = (desc.tx, desc.ty, desc.tz)
+        self._desc = desc
+
+    def matrix_bytes(self):
+        """Bytes of operator data streamed per application (the kappa tile field)."""
+        return 0 if self.field is None else 8 * self.field.numel()
+
+    def node_kappa(self):
+        """Full node-kappa array (host), x fastest."""
+        if self.field_host is None:
+            return np.full(self.n, self._desc.kconst)
+        f = self.field_host
+        idx = [np.arange(s) // t for s, t in zip(self.shape, self.tile)]
+        if self.dim == 2:
+            return f[idx[1][:, None], idx[0][None, :]].reshape(-1)
+        return f[idx[2][:, None, None], idx[1][None, :, None], idx[0][None, None, :]].reshape(-1)
+
+    def to_csr(self):
+        """Host CSR of the same operator (bitwise the reference generator's)."""
+        from .problems import diffusion_csr
+        return diffusion_csr(self.shape, self.node_kappa(), self.axis_coef)
+
+    def apply(self, X, ldx, Y, ldy, m, live=None, stream=None):
+        st = current_stream_ptr(self.device) if stream is None else stream
+        _lib.call("ekcg_spmm_stencil", ctypes.byref(self._desc), _ptr(X), ldx, _ptr(Y), ldy, m, live, st)
+
+
+def as_operator(A, device=None):
+    if isinstance(A, (CsrOperator, StencilOperator)):
+        return A
+    if hasattr(A, "row_ptr") and hasattr(A, "col_idx") and hasattr(A, "values"):
+        return CsrOperator(A, device)
+    raise TypeError(f"unsupported operator type {type(A).__name__}")

@@ -1,0 +1,57 @@
+"""Shared fixtures.  `-m gpu` tests need a CUDA device; everything else runs on CPU."""
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+GOLDEN = ROOT / "tests" / "golden"
+sys.path.insert(0, str(ROOT))
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+def _cuda_available():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def pytest_collection_modifyitems(config, items):
+    if _cuda_available():
+        return
+    skip = pytest.mark.skip(reason="no CUDA device")
+    for item in items:
+        if "gpu" in item.keywords:
+            item.add_marker(skip)
+
+
+@pytest.fixture(scope="session")
+def kernels_golden():
+    return dict(np.load(GOLDEN / "kernels.npz"))
+
+
+@pytest.fixture(scope="session")
+def solves_golden():
+    meta = json.loads((GOLDEN / "solves.json").read_text())
+    arrays = dict(np.load(GOLDEN / "solves.npz"))
+    return meta, arrays
+
+
+@pytest.fixture(scope="session")
+def generators_golden():
+    return json.loads((GOLDEN / "generators.json").read_text())
+
+
+def golden_case_inputs(arrays, name):
+    """(row_ptr, col_idx, values, b, owner, x0) stored for a small golden case."""
+    g = lambda k: arrays.get(f"{name}__{k}")
+    return g("rp"), g("ci"), g("vals"), g("b"), g("owner"), g("x0")

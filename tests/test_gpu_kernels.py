@@ -1,0 +1,175 @@
+"""Kernel-level parity on the GPU, through the C ABI (paper_2305_19013_b200._lib).
+
+Integer/copy work (split) and the sparse products are bit-exact against the
+reference's outputs; fp64 Gram/update/factorization kernels are compared with
+a torch fp64 / numpy reference at the stated tolerances.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_19013_b200 as pk
+from paper_2305_19013_b200 import _lib
+from paper_2305_19013_b200.problems import make_config
+from oracle import ekcg_oracle as orc
+
+DEV = "cuda"
+
+
+def dev(a, dtype=torch.float64):
+    return torch.as_tensor(np.ascontiguousarray(a)).to(DEV, dtype)
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def test_split_bitwise(kernels_golden):
+    g = kernels_golden
+    p = pk.Partition.from_owner(g["split_owner"], 3)
+    W = p.split(g["split_v"])
+    assert np.array_equal(W, g["split_W"])
+    rng = np.random.default_rng(3)
+    owner = rng.integers(0, 16, 100_003)
+    owner[:16] = np.arange(16)
+    v = rng.standard_normal(owner.size)
+    v[::7] = -0.0
+    q = pk.Partition.from_owner(owner, 16)
+    Wd = q.split(v)
+    ref = orc.split_block(owner, 16, v)
+    assert np.array_equal(Wd.view(np.int64), ref.view(np.int64))  # bitwise incl. signed zeros
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_csr_spmm_bitwise(kernels_golden, tag):
+    g = kernels_golden
+    A = pk.SparseSpdMatrix(len(g[f"spmm_{tag}_rp"]) - 1, g[f"spmm_{tag}_rp"], g[f"spmm_{tag}_ci"],
+                           g[f"spmm_{tag}_v"])
+    X = g[f"spmm_{tag}_X"]
+    assert np.array_equal(pk.spmm(A, X), g[f"spmm_{tag}_Y"])
+    assert np.array_equal(pk.spmv(A, X[:, 3].copy()), g[f"spmv_{tag}_y"])
+    for m in (1, 3, 8, 16, 64):
+        assert np.array_equal(pk.spmm(A, X[:, :m].copy()), g[f"spmm_{tag}_Y"][:, :m])
+
+
+@pytest.mark.parametrize("idx,edge", [(1, 20), (2, 8), (3, 16), (4, 8), (5, 64)])
+@pytest.mark.parametrize("m", [1, 2, 7, 16, 32])
+def test_stencil_equals_csr_bitwise(idx, edge, m):
+    prob = make_config(idx, edge)
+    A = prob.csr()
+    op = prob.stencil()
+    X = np.random.default_rng(idx * 100 + m).standard_normal((prob.n, m))
+    X[::5, 0] = 0.0
+    Xd = dev(X)
+    Yd = torch.empty_like(Xd)
+    op.apply(Xd, m, Yd, m, m)
+    ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, X)
+    assert np.array_equal(Yd.cpu().numpy(), ref)
+    assert np.array_equal(pk.spmm(A, X), ref)
+
+
+def test_spmm_strided_slabs():
+    prob = make_config(2, 8)
+    op = prob.stencil()
+    A = prob.csr()
+    n, t, s = prob.n, 4, 3
+    V = torch.zeros((n, s * t), dtype=torch.float64, device=DEV)
+    V[:, :t] = dev(np.random.default_rng(1).standard_normal((n, t)))
+    for i in range(1, s):
+        op.apply(V.data_ptr() + 8 * (i - 1) * t, s * t, V.data_ptr() + 8 * i * t, s * t, t)
+    Vh = V.cpu().numpy()
+    ref = Vh[:, :t]
+    for i in range(1, s):
+        ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, ref)
+        assert np.array_equal(Vh[:, i * t:(i + 1) * t], ref)
+
+
+@pytest.mark.parametrize("m1,m2", [(1, 1), (3, 1), (5, 7), (8, 8), (16, 16), (32, 32), (64, 64), (16, 1),
+                                   (20, 20), (64, 32)])
+@pytest.mark.parametrize("n", [1, 37, 4099, 200_000])
+def test_gram_multi_block(m1, m2, n):
+    rng = np.random.default_rng(m1 * 1000 + m2 + n)
+    d = 3
+    Xs = [dev(rng.standard_normal((n, m1))) for _ in range(d)]
+    Y = dev(rng.standard_normal((n, m2)))
+    tab = torch.tensor([x.data_ptr() for x in Xs], dtype=torch.int64, device=DEV)
+    chunks = _lib.query("ekcg_gram_chunks", n, d, m1, m2)
+    part = torch.empty(chunks * d * m1 * m2, dtype=torch.float64, device=DEV)
+    out = torch.empty(d * m1 * m2, dtype=torch.float64, device=DEV)
+    _lib.call("ekcg_gram", tab.data_ptr(), m1, d, m1, Y.data_ptr(), m2, m2, n, part.data_ptr(), None, stream())
+    _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m1 * m2, out.data_ptr(), None, stream())
+    got = out.view(d, m1, m2)
+    for i in range(d):
+        ref = Xs[i].T @ Y
+        scale = (Xs[i].abs().T @ Y.abs()).max().item() + 1e-300
+        assert (got[i] - ref).abs().max().item() <= 1e-13 * scale
+
+
+def test_gram_deterministic():
+    rng = np.random.default_rng(9)
+    X = rng.standard_normal((300_001, 16))
+    a = pk.gram(X, X)
+    b = pk.gram(X, X)
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("m1,m2", [(4, 4), (8, 8), (16, 16), (32, 32), (64, 64), (16, 8), (6, 6)])
+@pytest.mark.parametrize("n", [5, 1000, 100_003])
+@pytest.mark.parametrize("beta", [0.0, 1.0])
+def test_block_update(m1, m2, n, beta):
+    rng = np.random.default_rng(n + m1 * 7 + m2)
+    d = 4
+    Qs = [dev(rng.standard_normal((n, m1))) for _ in range(d)]
+    C = dev(rng.standard_normal((d * m1, m2)))
+    Win = dev(rng.standard_normal((n, m2)))
+    Wout = torch.empty_like(Win)
+    tab = torch.tensor([q.data_ptr() for q in Qs], dtype=torch.int64, device=DEV)
+    _lib.call("ekcg_block_update", tab.data_ptr(), m1, d, m1, C.data_ptr(), Win.data_ptr() if beta else None,
+              m2, Wout.data_ptr(), m2, m2, beta, -1.0, n, None, stream())
+    ref = beta * Win - sum(Qs[i] @ C[i * m1:(i + 1) * m1] for i in range(d))
+    scale = sum((Qs[i].abs() @ C[i * m1:(i + 1) * m1].abs()) for i in range(d)).max().item() + 1.0
+    assert (Wout - ref).abs().max().item() <= 1e-13 * scale
+    # in place (Wout aliases Win), the CGS2 second pass
+    if beta:
+        W2 = Win.clone()
+        _lib.call("ekcg_block_update", tab.data_ptr(), m1, d, m1, C.data_ptr(), W2.data_ptr(), m2, W2.data_ptr(),
+                  m2, m2, 1.0, -1.0, n, None, stream())
+        assert torch.equal(W2, Wout)
+
+
+@pytest.mark.parametrize("m", [1, 2, 6, 16, 64])
+def test_cholesky_and_trsm(m):
+    rng = np.random.default_rng(m)
+    W = rng.standard_normal((3 * m + 5, m))
+    B = W.T @ W
+    R = pk.cholesky_small(B)
+    ref = orc.small_cholesky(B)
+    assert np.allclose(R, ref, rtol=1e-11, atol=1e-12 * np.abs(ref).max())
+    assert np.allclose(R.T @ R, B, rtol=1e-12, atol=1e-12 * np.abs(B).max())
+    X = rng.standard_normal((50, m))
+    Y = pk.trsm_right_inv(X, R)
+    assert np.allclose(Y @ R, X, rtol=1e-12, atol=1e-11)
+
+
+def test_cholesky_known_answer_and_breakdown(kernels_golden):
+    R = pk.cholesky_small(np.array([[4.0, 2.0], [2.0, 5.0]]))
+    assert np.array_equal(R, np.array([[2.0, 1.0], [0.0, 2.0]]))
+    with pytest.raises(pk.Breakdown, match="pivot .* at column 1"):
+        pk.cholesky_small(np.array([[1.0, 1.0], [1.0, 1.0]]))
+
+
+def test_norm_and_gram_api(kernels_golden):
+    g = kernels_golden
+    G = pk.gram(g["gram_X"], g["gram_Y"])
+    assert np.allclose(G, g["gram_G"], rtol=1e-13, atol=1e-13)
+    v = np.random.default_rng(0).standard_normal(12345)
+    assert abs(pk.norm2(v) - np.linalg.norm(v)) <= 1e-14 * np.linalg.norm(v)
+
+
+def test_launch_counter_moves():
+    before = _lib.query("ekcg_launch_count")
+    pk.norm2(np.ones(10))
+    assert _lib.query("ekcg_launch_count") >= before + 2
