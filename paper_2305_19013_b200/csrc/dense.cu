@@ -27,9 +27,22 @@ long long rows_per_chunk(long long n, int chunks) {
     return ((r + 15) / 16) * 16;
 }
 
-int gram_chunks(long long n, int d) {
-    const long long target = 148LL * 8;  // ~8 CTAs per SM in total
-    long long p = (target + d - 1) / d;
+// Blocks per CTA that share one pass over Y (see gram_dmma_kernel).
+int gram_blocks_per_cta(int m1, int m2) {
+    if (m1 != m2) return 1;
+    switch (m1) {
+        case 8: return 8;
+        case 16: return 4;
+        case 32: return 2;
+        default: return 1;
+    }
+}
+
+int gram_chunks(long long n, int d, int m1, int m2) {
+    const int gb = gram_blocks_per_cta(m1, m2);
+    const long long groups = (d + gb - 1) / gb;
+    const long long target = 148LL * 4;  // one wave at ~4 resident CTAs per SM
+    long long p = (target + groups - 1) / groups;
     long long max_p = (n + 255) / 256;
     if (p > max_p) p = max_p;
     if (p < 1) p = 1;
@@ -38,18 +51,20 @@ int gram_chunks(long long n, int d) {
 
 // ---------------------------------------------------------------------------
 // DMMA Gram: partials[p][i] (M x M) = X_i[rows of p]^T Y[rows of p]
-// Warp w: row lane ks = w % KS, output quadrant q = w / KS with TA x TB
-// tiles of 8x8.  Rows advance in k-steps of 4 (the mma K).
+// CTA (p, g) handles row chunk p for blocks i = g*GB .. g*GB+GB-1, so each Y
+// fragment loaded feeds GB blocks.  Warp w: row lane ks = w % KS, output
+// quadrant q = w / KS with TA x TB tiles of 8x8.  Rows advance in k-steps of
+// 4 (the mma K); fragments come straight from the row-major blocks.
 // ---------------------------------------------------------------------------
-template <int M, int TA, int TB, int KS, int U>
+template <int M, int TA, int TB, int KS, int U, int GB>
 __global__ void __launch_bounds__(kGramThreads)
-gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, const double* __restrict__ Y, int ldy,
+gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const double* __restrict__ Y, int ldy,
                  long long n, long long rows_chunk, double* __restrict__ partials,
                  const int* __restrict__ live) {
     EKCG_GATE(live);
     static_assert((M / 8 / TA) * (M / 8 / TB) * KS == kGramThreads / 32, "warp layout");
     constexpr int QA = M / 8 / TA;
-    __shared__ double red[KS > 1 ? KS * M * M : 1];
+    __shared__ double red[KS > 1 ? KS * GB * M * M : 1];
 
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -57,70 +72,88 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, const double* __
     const int quad = warp / KS;
     const int a_base = (quad % QA) * TA * 8;
     const int b_base = (quad / QA) * TB * 8;
-    const int i = blockIdx.y;
-    const double* __restrict__ X = Xs[i];
+    const int i0 = blockIdx.y * GB;
+    const int nb = min(GB, d - i0);
+    const double* __restrict__ X[GB];
+#pragma unroll
+    for (int g = 0; g < GB; ++g) X[g] = Xs[min(i0 + g, d - 1)];
     const long long r0 = blockIdx.x * rows_chunk;
     long long r1 = r0 + rows_chunk;
     if (r1 > n) r1 = n;
     const long long steps = (r1 > r0) ? (r1 - r0 + 3) / 4 : 0;
 
-    double acc[TA][TB][2];
+    double acc[GB][TA][TB][2];
 #pragma unroll
-    for (int ta = 0; ta < TA; ++ta)
+    for (int g = 0; g < GB; ++g)
 #pragma unroll
-        for (int tb = 0; tb < TB; ++tb) acc[ta][tb][0] = acc[ta][tb][1] = 0.0;
+        for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+            for (int tb = 0; tb < TB; ++tb) acc[g][ta][tb][0] = acc[g][ta][tb][1] = 0.0;
 
     const int lr = lane & 3;
     const int lc = lane >> 2;
     for (long long s0 = ks; s0 < steps; s0 += (long long)KS * U) {
-        double af[U][TA], bf[U][TB];
+        double af[U][GB][TA], bf[U][TB];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             long long s = s0 + (long long)u * KS;
             long long r = r0 + 4 * s + lr;
             bool ok = (s < steps) && (r < r1);
-            const double* xrow = X + r * ldx + a_base + lc;
             const double* yrow = Y + r * ldy + b_base + lc;
 #pragma unroll
-            for (int ta = 0; ta < TA; ++ta) af[u][ta] = ok ? __ldg(xrow + 8 * ta) : 0.0;
-#pragma unroll
             for (int tb = 0; tb < TB; ++tb) bf[u][tb] = ok ? __ldg(yrow + 8 * tb) : 0.0;
+#pragma unroll
+            for (int g = 0; g < GB; ++g) {
+                const double* xrow = X[g] + r * ldx + a_base + lc;
+                bool okg = ok && (g < nb);
+#pragma unroll
+                for (int ta = 0; ta < TA; ++ta) af[u][g][ta] = okg ? __ldg(xrow + 8 * ta) : 0.0;
+            }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
 #pragma unroll
-            for (int ta = 0; ta < TA; ++ta)
+            for (int g = 0; g < GB; ++g)
 #pragma unroll
-                for (int tb = 0; tb < TB; ++tb) dmma_8x8x4(acc[ta][tb], af[u][ta], bf[u][tb]);
+                for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+                    for (int tb = 0; tb < TB; ++tb) dmma_8x8x4(acc[g][ta][tb], af[u][g][ta], bf[u][tb]);
     }
 
-    double* out = partials + ((long long)blockIdx.x * gridDim.y + i) * (M * M);
     if (KS == 1) {
 #pragma unroll
-        for (int ta = 0; ta < TA; ++ta)
+        for (int g = 0; g < GB; ++g) {
+            if (g >= nb) break;
+            double* out = partials + ((long long)blockIdx.x * d + i0 + g) * (M * M);
 #pragma unroll
-            for (int tb = 0; tb < TB; ++tb) {
-                int a = a_base + 8 * ta + lc;
-                int b = b_base + 8 * tb + 2 * lr;
-                out[a * M + b] = acc[ta][tb][0];
-                out[a * M + b + 1] = acc[ta][tb][1];
-            }
+            for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+                for (int tb = 0; tb < TB; ++tb) {
+                    int a = a_base + 8 * ta + lc;
+                    int b = b_base + 8 * tb + 2 * lr;
+                    out[a * M + b] = acc[g][ta][tb][0];
+                    out[a * M + b + 1] = acc[g][ta][tb][1];
+                }
+        }
     } else {
 #pragma unroll
-        for (int ta = 0; ta < TA; ++ta)
+        for (int g = 0; g < GB; ++g)
 #pragma unroll
-            for (int tb = 0; tb < TB; ++tb) {
-                int a = a_base + 8 * ta + lc;
-                int b = b_base + 8 * tb + 2 * lr;
-                red[(ks * M + a) * M + b] = acc[ta][tb][0];
-                red[(ks * M + a) * M + b + 1] = acc[ta][tb][1];
-            }
+            for (int ta = 0; ta < TA; ++ta)
+#pragma unroll
+                for (int tb = 0; tb < TB; ++tb) {
+                    int a = a_base + 8 * ta + lc;
+                    int b = b_base + 8 * tb + 2 * lr;
+                    red[((ks * GB + g) * M + a) * M + b] = acc[g][ta][tb][0];
+                    red[((ks * GB + g) * M + a) * M + b + 1] = acc[g][ta][tb][1];
+                }
         __syncthreads();
-        for (int o = threadIdx.x; o < M * M; o += kGramThreads) {
-            double s = red[o];
+        for (int o = threadIdx.x; o < nb * M * M; o += kGramThreads) {
+            const int g = o / (M * M), e = o % (M * M);
+            double s = red[g * M * M + e];
 #pragma unroll
-            for (int k = 1; k < KS; ++k) s += red[k * M * M + o];
-            out[o] = s;
+            for (int k = 1; k < KS; ++k) s += red[(k * GB + g) * M * M + e];
+            partials[((long long)blockIdx.x * d + i0 + g) * (M * M) + e] = s;
         }
     }
 }
@@ -358,31 +391,30 @@ __global__ void sub_kernel(const double* __restrict__ a, const double* __restric
 // C ABI
 // ---------------------------------------------------------------------------
 extern "C" int ekcg_gram_chunks(long long n, int d, int m1, int m2) {
-    (void)m1;
-    (void)m2;
-    if (n < 1 || d < 1) return 1;
-    return gram_chunks(n, d);
+    if (n < 1 || d < 1 || m1 < 1 || m2 < 1) return 1;
+    return gram_chunks(n, d, m1, m2);
 }
 
 extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2,
                          long long n, double* partials, const int* live, void* stream) {
     if (d < 1 || m1 < 1 || m2 < 1 || ldx < m1 || ldy < m2 || n < 1) return EKCG_EINVAL;
-    const int chunks = gram_chunks(n, d);
+    const int chunks = gram_chunks(n, d, m1, m2);
     const long long rc = rows_per_chunk(n, chunks);
-    dim3 grid(chunks, d);
+    const int gb = gram_blocks_per_cta(m1, m2);
+    dim3 grid(chunks, (d + gb - 1) / gb);
     cudaStream_t st = as_stream(stream);
     if (m1 == m2 && m1 == 8) {
-        gram_dmma_kernel<8, 1, 1, 4, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+        gram_dmma_kernel<8, 1, 1, 4, 2, 8><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else if (m1 == m2 && m1 == 16) {
-        gram_dmma_kernel<16, 2, 2, 4, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+        gram_dmma_kernel<16, 2, 2, 4, 2, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else if (m1 == m2 && m1 == 32) {
-        gram_dmma_kernel<32, 4, 2, 2, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+        gram_dmma_kernel<32, 4, 2, 2, 2, 2><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else if (m1 == m2 && m1 == 64) {
-        gram_dmma_kernel<64, 4, 4, 1, 2><<<grid, kGramThreads, 0, st>>>(Xs, ldx, Y, ldy, n, rc, partials, live);
+        gram_dmma_kernel<64, 4, 4, 1, 2, 1><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else {
         const int O = m1 * m2;
         size_t smem = (O <= 256) ? sizeof(double) * 256 : 0;
-        gram_generic_kernel<<<grid, 256, smem, st>>>(Xs, ldx, m1, Y, ldy, m2, n, rc, partials, live);
+        gram_generic_kernel<<<dim3(chunks, d), 256, smem, st>>>(Xs, ldx, m1, Y, ldy, m2, n, rc, partials, live);
     }
     ++g_ekcg_launches;
     return launch_status();

@@ -121,6 +121,7 @@ class DeviceEngine:
         self.C = torch.empty(1 << 12, **f64)
         self.ctrl = torch.zeros(_lib.query("ekcg_ctrl_bytes"), dtype=torch.uint8, device=dev)
         self.ctrl_host = torch.empty(self.ctrl.numel(), dtype=torch.uint8, pin_memory=True)
+        self.snap_bufs = [torch.empty(self.ctrl.numel(), dtype=torch.uint8, pin_memory=True) for _ in range(3)]
         self.live = self.ctrl.data_ptr()
         self.history = torch.zeros(min(self.kmax, 4096) + 1, **f64)
         self.checks = torch.zeros(max(1, min(self.kmax, 4096) // self.every + 1), **f64)
@@ -144,17 +145,18 @@ class DeviceEngine:
             setattr(self, name, buf)
         return buf
 
-    def _chunks(self, d):
-        c = self.gram_chunks.get(d)
+    def _chunks(self, d, m1, m2):
+        key = (d, m1, m2)
+        c = self.gram_chunks.get(key)
         if c is None:
-            c = _lib.query("ekcg_gram_chunks", self.n, d, 1, 1)
-            self.gram_chunks[d] = c
+            c = _lib.query("ekcg_gram_chunks", self.n, d, m1, m2)
+            self.gram_chunks[key] = c
         return c
 
     # ---------------------------------------------------------- primitives
     def _gram(self, xs_addr, ldx, d, m1, y_ptr, ldy, m2, out_ptr, tag="gram"):
         """out (d*m1*m2) = [X_i^T Y] via split-K partials + fixed-order reduce."""
-        chunks = self._chunks(d)
+        chunks = self._chunks(d, m1, m2)
         part = self._ensure("part", chunks * d * m1 * m2)
         run = lambda: _lib.call("ekcg_gram", xs_addr, ldx, d, m1, y_ptr, ldy, m2, self.n, part.data_ptr(),
                                 self.live, self.stream)
@@ -368,6 +370,19 @@ class DeviceEngine:
             "last_rho": float(dbl[5]),
         }
 
+    def _snapshot(self, j):
+        buf = self.snap_bufs[j % len(self.snap_bufs)]
+        buf.copy_(self.ctrl, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        return buf, ev
+
+    def _wait_snapshot(self, snap):
+        buf, ev = snap
+        ev.synchronize()
+        ints = buf.numpy()[:32].view(np.int32)
+        return {"live": int(ints[0]), "status": int(ints[1]), "k_done": int(ints[2])}
+
     # ---------------------------------------------------------------- solve
     def solve(self, b, x0=None, x_star=None, on_iteration=None):
         cfg = self.cfg
@@ -402,6 +417,7 @@ class DeviceEngine:
         lookahead = 1
         tol1 = 1.0
         ctrl = None
+        snaps = []
         while k <= self.kmax:
             if sync_each:
                 self._enqueue_iteration(k, tol1)
@@ -416,17 +432,21 @@ class DeviceEngine:
                     break
                 k += 1
             else:
+                # run ahead: snapshot the control block after every batch and
+                # only wait for the PREVIOUS batch's snapshot, so the GPU queue
+                # never drains while the host polls
                 for _ in range(lookahead):
                     if k > self.kmax:
                         break
                     self._enqueue_iteration(k, 1.0)
                     k += 1
-                ctrl = self._read_ctrl()
-                if ctrl["live"] == 0:
-                    break
+                snaps.append(self._snapshot(len(snaps)))
+                if len(snaps) >= 2:
+                    prev = self._wait_snapshot(snaps[-2])
+                    if prev["live"] == 0:
+                        break
                 lookahead = min(2 * lookahead, self.max_lookahead)
-        if ctrl is None:
-            ctrl = self._read_ctrl()
+        ctrl = self._read_ctrl()  # after a full sync: the final state
         ev1.record()
         ev1.synchronize()
         solve_s = ev0.elapsed_time(ev1) / 1e3

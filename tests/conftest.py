@@ -47,6 +47,12 @@ def solves_golden():
 
 
 @pytest.fixture(scope="session")
+def floors_golden():
+    """Reference-vs-reference reordering floors (tests/golden/make_floors.py)."""
+    return json.loads((GOLDEN / "floors.json").read_text())
+
+
+@pytest.fixture(scope="session")
 def generators_golden():
     return json.loads((GOLDEN / "generators.json").read_text())
 
