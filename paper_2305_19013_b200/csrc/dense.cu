@@ -28,18 +28,21 @@ long long rows_per_chunk(long long n, int chunks) {
 }
 
 // Blocks per CTA that share one pass over Y (see gram_dmma_kernel).
-int gram_blocks_per_cta(int m1, int m2) {
+int gram_blocks_per_cta(int d, int m1, int m2) {
     if (m1 != m2) return 1;
+    int gb = 1;
     switch (m1) {
-        case 8: return 8;
-        case 16: return 4;
-        case 32: return 2;
-        default: return 1;
+        case 8: gb = 8; break;
+        case 16: gb = 4; break;
+        case 32: gb = 2; break;
+        default: gb = 1;
     }
+    while (gb > 1 && gb / 2 >= d) gb /= 2;  // d = 1 -> 1, d = 2 -> 2, ...
+    return gb;
 }
 
 int gram_chunks(long long n, int d, int m1, int m2) {
-    const int gb = gram_blocks_per_cta(m1, m2);
+    const int gb = gram_blocks_per_cta(d, m1, m2);
     const long long groups = (d + gb - 1) / gb;
     const long long target = 148LL * 4;  // one wave at ~4 resident CTAs per SM
     long long p = (target + groups - 1) / groups;
@@ -199,14 +202,37 @@ gram_generic_kernel(const double* const* __restrict__ Xs, int ldx, int m1, const
     }
 }
 
-__global__ void reduce_kernel(const double* __restrict__ partials, int chunks, long long len,
-                              double* __restrict__ out, const int* __restrict__ live) {
+// out[j] = sum_p partials[p*len + j].  Block = W warps x 32 lanes; lane owns
+// output j = 32*blockIdx.x + lane, warp w sums p = w, w+W, ... (4 loads in
+// flight), then the W warp sums are combined in fixed order: deterministic.
+__global__ void __launch_bounds__(1024)
+reduce_kernel(const double* __restrict__ partials, int chunks, long long len, double* __restrict__ out,
+              const int* __restrict__ live) {
     EKCG_GATE(live);
-    for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < len;
-         j += (long long)gridDim.x * blockDim.x) {
-        double s = partials[j];
-        for (int p = 1; p < chunks; ++p) s += partials[(long long)p * len + j];
-        out[j] = s;
+    __shared__ double ws[32][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const long long j = (long long)blockIdx.x * 32 + lane;
+    double s = 0.0;
+    if (j < len) {
+        int p = warp;
+        for (; p + 3 * W < chunks; p += 4 * W) {
+            double a = partials[(long long)p * len + j];
+            double b = partials[(long long)(p + W) * len + j];
+            double c = partials[(long long)(p + 2 * W) * len + j];
+            double d = partials[(long long)(p + 3 * W) * len + j];
+            s += a;
+            s += b;
+            s += c;
+            s += d;
+        }
+        for (; p < chunks; p += W) s += partials[(long long)p * len + j];
+    }
+    ws[warp][lane] = s;
+    __syncthreads();
+    if (warp == 0 && j < len) {
+        double t = ws[0][lane];
+        for (int w = 1; w < W; ++w) t += ws[w][lane];
+        out[j] = t;
     }
 }
 
@@ -324,6 +350,9 @@ __device__ __forceinline__ double block_sum(double v) {
     return s;  // valid in thread 0
 }
 
+// L lanes cooperate on one row (L = power of two <= 32): coalesced reads of
+// the row-major W / AW rows, shuffle reduction of the row dot products.
+template <int L>
 __global__ void __launch_bounds__(kVecThreads)
 xr_update_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ AW, int ldaw,
                  const double* __restrict__ alpha, int m, double* __restrict__ x, double* __restrict__ r,
@@ -332,20 +361,34 @@ xr_update_kernel(const double* __restrict__ W, int ldw, const double* __restrict
     __shared__ double sa[256];
     for (int a = threadIdx.x; a < m && a < 256; a += blockDim.x) sa[a] = alpha[a];
     __syncthreads();
+    constexpr int RPW = 32 / L;  // rows per warp pass
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / L, li = lane % L;
+    const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long warps_total = ((long long)gridDim.x * blockDim.x) >> 5;
     double sq = 0.0;
-    for (long long row = blockIdx.x * (long long)blockDim.x + threadIdx.x; row < n;
-         row += (long long)gridDim.x * blockDim.x) {
-        const double* w = W + row * ldw;
-        const double* aw = AW + row * ldaw;
+    for (long long base = warp_global * RPW; base < n; base += warps_total * RPW) {
+        const long long row = base + sub;
         double dx = 0.0, dr = 0.0;
-        for (int a = 0; a < m; ++a) {
-            dx += w[a] * sa[a];
-            dr += aw[a] * sa[a];
+        if (row < n) {
+            const double* w = W + row * ldw;
+            const double* aw = AW + row * ldaw;
+            for (int a = li; a < m; a += L) {
+                dx += w[a] * sa[a];
+                dr += aw[a] * sa[a];
+            }
         }
-        x[row] = x[row] + dx;
-        double rn = r[row] - dr;
-        r[row] = rn;
-        sq += rn * rn;
+#pragma unroll
+        for (int off = L / 2; off > 0; off >>= 1) {
+            dx += __shfl_xor_sync(0xffffffffu, dx, off);
+            dr += __shfl_xor_sync(0xffffffffu, dr, off);
+        }
+        if (row < n && li == 0) {
+            x[row] = x[row] + dx;
+            double rn = r[row] - dr;
+            r[row] = rn;
+            sq += rn * rn;
+        }
     }
     double s = block_sum(sq);
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
@@ -400,17 +443,25 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     if (d < 1 || m1 < 1 || m2 < 1 || ldx < m1 || ldy < m2 || n < 1) return EKCG_EINVAL;
     const int chunks = gram_chunks(n, d, m1, m2);
     const long long rc = rows_per_chunk(n, chunks);
-    const int gb = gram_blocks_per_cta(m1, m2);
+    const int gb = gram_blocks_per_cta(d, m1, m2);
     dim3 grid(chunks, (d + gb - 1) / gb);
     cudaStream_t st = as_stream(stream);
+#define GRAM_LAUNCH(M, TA, TB, KS, U, GB) \
+    gram_dmma_kernel<M, TA, TB, KS, U, GB><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live)
     if (m1 == m2 && m1 == 8) {
-        gram_dmma_kernel<8, 1, 1, 4, 2, 8><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
+        if (gb == 8) GRAM_LAUNCH(8, 1, 1, 4, 4, 8);
+        else if (gb == 4) GRAM_LAUNCH(8, 1, 1, 4, 4, 4);
+        else if (gb == 2) GRAM_LAUNCH(8, 1, 1, 4, 4, 2);
+        else GRAM_LAUNCH(8, 1, 1, 4, 4, 1);
     } else if (m1 == m2 && m1 == 16) {
-        gram_dmma_kernel<16, 2, 2, 4, 2, 4><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
+        if (gb == 4) GRAM_LAUNCH(16, 2, 2, 4, 2, 4);
+        else if (gb == 2) GRAM_LAUNCH(16, 2, 2, 4, 2, 2);
+        else GRAM_LAUNCH(16, 2, 2, 4, 4, 1);
     } else if (m1 == m2 && m1 == 32) {
-        gram_dmma_kernel<32, 4, 2, 2, 2, 2><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
+        if (gb == 2) GRAM_LAUNCH(32, 4, 2, 2, 2, 2);
+        else GRAM_LAUNCH(32, 4, 2, 2, 4, 1);
     } else if (m1 == m2 && m1 == 64) {
-        gram_dmma_kernel<64, 4, 4, 1, 2, 1><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
+        GRAM_LAUNCH(64, 4, 4, 1, 2, 1);
     } else {
         const int O = m1 * m2;
         size_t smem = (O <= 256) ? sizeof(double) * 256 : 0;
@@ -423,7 +474,10 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
 extern "C" int ekcg_reduce(const double* partials, int chunks, long long len, double* out, const int* live,
                            void* stream) {
     if (chunks < 1 || len < 1) return EKCG_EINVAL;
-    reduce_kernel<<<grid_for(len, 256), 256, 0, as_stream(stream)>>>(partials, chunks, len, out, live);
+    int warps = chunks < 32 ? chunks : 32;
+    long long blocks = (len + 31) / 32;
+    // keep enough warps in flight when there are few outputs
+    reduce_kernel<<<(unsigned)blocks, 32 * warps, 0, as_stream(stream)>>>(partials, chunks, len, out, live);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -466,8 +520,16 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
                               double* x, double* r, long long n, double* rho2_partials, const int* live,
                               void* stream) {
     if (m < 1 || m > 256 || ldw < m || ldaw < m || n < 1) return EKCG_EINVAL;
-    xr_update_kernel<<<vec_chunks(n), kVecThreads, 0, as_stream(stream)>>>(W, ldw, AW, ldaw, alpha, m, x, r, n,
-                                                                          rho2_partials, live);
+    cudaStream_t st = as_stream(stream);
+    const int g = vec_chunks(n);
+#define XR_LAUNCH(L) xr_update_kernel<L><<<g, kVecThreads, 0, st>>>(W, ldw, AW, ldaw, alpha, m, x, r, n, rho2_partials, live)
+    if (m >= 32) XR_LAUNCH(32);
+    else if (m >= 16) XR_LAUNCH(16);
+    else if (m >= 8) XR_LAUNCH(8);
+    else if (m >= 4) XR_LAUNCH(4);
+    else if (m >= 2) XR_LAUNCH(2);
+    else XR_LAUNCH(1);
+#undef XR_LAUNCH
     ++g_ekcg_launches;
     return launch_status();
 }
