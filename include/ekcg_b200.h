@@ -122,6 +122,38 @@ int ekcg_cholinv(const double* G, int m, double* S, void* ctrl, int iteration, d
  * cholesky_small (linalg.py:164-184). */
 int ekcg_cholesky(const double* B, int m, double tol, double* R, double* info, void* stream);
 
+/* ---- fused iteration kernels (m in {8,16,32,64}) -------------------------
+ * Each reduces its split-K partials in-kernel (last CTA to arrive, fixed
+ * order) and runs the m x m factor / bookkeeping there.  `partials` holds
+ * ekcg_fused_partials(n, m) doubles; `counter` is a device uint32 that must be
+ * 0 before the first call (the kernels leave it 0). */
+int ekcg_fused_partials(long long n, int m);
+
+/* Wout = Win - sum_i Q_i C_i (CGS2 pass 2, aortho.py:93-94) fused with
+ * Graw = Wout^T Wout and the Pre-CholQR factor S0 (aortho.py:104-106). */
+int ekcg_update_prechol(const double* const* Qs, int ldq, int d, const double* C, const double* Win, int ldwi,
+                        double* Wout, int ldwo, int m, long long n, double* partials, unsigned int* counter,
+                        double* S0, void* ctrl, int iteration, double tol, void* stream);
+
+/* Wout = Q_0 S (W_k = W0 R^-1, linalg.py:187-196) fused with vout = Wout^T vec
+ * (alpha = W^T r, solvers.py:394). */
+int ekcg_update_vec(const double* const* Qs, int ldq, const double* S, double* Wout, int ldwo, int m, long long n,
+                    const double* vec, double* partials, unsigned int* counter, double* vout, void* ctrl,
+                    void* stream);
+
+/* G = X^T (A X) for the stencil operator without materialising A X, fused
+ * with the A-CholQR factor S = chol(sym G)^-1 (aortho.py:107-109). ldx == m. */
+int ekcg_stencil_cholinv(const EkcgStencil* desc, const double* X, int ldx, int m, double* partials,
+                         unsigned int* counter, double* S, void* ctrl, int iteration, double tol, void* stream);
+
+/* Y = A X (written) fused with x += X alpha, r -= Y alpha, |r|^2 and, when
+ * do_finish, the end-of-iteration bookkeeping of ekcg_finish (else |r|^2 is
+ * stored to *rho2_out) -- solvers.py:394-415. */
+int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy, int m,
+                    const double* alpha, double* x, double* r, double* partials, unsigned int* counter, void* ctrl,
+                    int k, int kmax, int stagnation_window, double* history, int do_finish, double* rho2_out,
+                    void* stream);
+
 /* ---- engine bookkeeping ------------------------------------------------ */
 
 /* Size in bytes of the control block. */
@@ -138,6 +170,11 @@ int ekcg_finish(void* ctrl, const double* rho2, int k, int kmax, int stagnation_
 
 /* checks[slot] = sqrt(*rho2) when the solve is live (true residual log, solvers.py:401-402). */
 int ekcg_store_norm(const double* rho2, double* checks, int slot, const int* live, void* stream);
+
+/* Performance knobs (results are unchanged up to summation order):
+ * key 1 = m=16 Gram variant (-1 auto, 0..6), key 2 = target CTA count of the Gram grid (0 auto).
+ * Call before a solve; ekcg_gram_chunks reflects the setting. */
+int ekcg_tune(int key, long long value);
 
 /* Kernel launches issued through this library since load. */
 unsigned long long ekcg_launch_count(void);

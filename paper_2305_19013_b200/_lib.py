@@ -41,6 +41,17 @@ SIGNATURES = {
     "ekcg_finish": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     "ekcg_store_norm": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "ekcg_launch_count": (c_uint64, []),
+    "ekcg_tune": (c_int, [c_int, c_longlong]),
+    "ekcg_fused_partials": (c_int, [c_longlong, c_int]),
+    "ekcg_update_prechol": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int,
+                                    c_longlong, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_double, c_void_p]),
+    "ekcg_update_vec": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_longlong, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_void_p]),
+    "ekcg_stencil_cholinv": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_int, c_double, c_void_p]),
+    "ekcg_stencil_xr": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
+                                c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p,
+                                c_void_p]),
 }
 
 

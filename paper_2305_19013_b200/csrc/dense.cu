@@ -27,13 +27,18 @@ long long rows_per_chunk(long long n, int chunks) {
     return ((r + 15) / 16) * 16;
 }
 
+// Tuning knobs (ekcg_tune): m = 16 Gram variant and target CTA count.
+int g_gram16_variant = -1;   // -1: automatic by d (measured on B200, tools/tune_gram.py)
+long long g_gram_target = 0;  // 0: automatic
+constexpr int kGram16GB[] = {4, 2, 2, 4, 4, 4, 1};
+
 // Blocks per CTA that share one pass over Y (see gram_dmma_kernel).
 int gram_blocks_per_cta(int d, int m1, int m2) {
     if (m1 != m2) return 1;
     int gb = 1;
     switch (m1) {
         case 8: gb = 8; break;
-        case 16: gb = 4; break;
+        case 16: gb = g_gram16_variant >= 0 ? kGram16GB[g_gram16_variant] : 4; break;
         case 32: gb = 2; break;
         default: gb = 1;
     }
@@ -44,7 +49,8 @@ int gram_blocks_per_cta(int d, int m1, int m2) {
 int gram_chunks(long long n, int d, int m1, int m2) {
     const int gb = gram_blocks_per_cta(d, m1, m2);
     const long long groups = (d + gb - 1) / gb;
-    const long long target = 148LL * 4;  // one wave at ~4 resident CTAs per SM
+    long long target = g_gram_target;
+    if (target <= 0) target = (m1 == 16 && m2 == 16 && d >= 48) ? 148LL * 8 : 148LL * 4;
     long long p = (target + groups - 1) / groups;
     long long max_p = (n + 255) / 256;
     if (p > max_p) p = max_p;
@@ -433,6 +439,18 @@ __global__ void sub_kernel(const double* __restrict__ a, const double* __restric
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
+extern "C" int ekcg_tune(int key, long long value) {
+    if (key == 1 && value >= -1 && value < (long long)(sizeof(kGram16GB) / sizeof(int))) {
+        g_gram16_variant = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 2 && value >= 0) {
+        g_gram_target = value;
+        return EKCG_OK;
+    }
+    return EKCG_EINVAL;
+}
+
 extern "C" int ekcg_gram_chunks(long long n, int d, int m1, int m2) {
     if (n < 1 || d < 1 || m1 < 1 || m2 < 1) return 1;
     return gram_chunks(n, d, m1, m2);
@@ -454,9 +472,14 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
         else if (gb == 2) GRAM_LAUNCH(8, 1, 1, 4, 4, 2);
         else GRAM_LAUNCH(8, 1, 1, 4, 4, 1);
     } else if (m1 == m2 && m1 == 16) {
-        if (gb == 4) GRAM_LAUNCH(16, 2, 2, 4, 2, 4);
+        const int v = g_gram16_variant >= 0 ? g_gram16_variant : (d >= 48 ? 0 : 3);
+        if (gb == 1) GRAM_LAUNCH(16, 2, 2, 4, 4, 1);
+        else if ((v == 1 || g_gram16_variant < 0) && gb == 2) GRAM_LAUNCH(16, 2, 2, 4, 4, 2);
         else if (gb == 2) GRAM_LAUNCH(16, 2, 2, 4, 2, 2);
-        else GRAM_LAUNCH(16, 2, 2, 4, 4, 1);
+        else if (v == 3 && gb == 4) GRAM_LAUNCH(16, 2, 2, 4, 1, 4);
+        else if (v == 5 && gb == 4) GRAM_LAUNCH(16, 2, 1, 2, 4, 4);
+        else if (v == 4 && gb == 4) GRAM_LAUNCH(16, 2, 2, 4, 4, 4);
+        else GRAM_LAUNCH(16, 2, 2, 4, 2, 4);
     } else if (m1 == m2 && m1 == 32) {
         if (gb == 2) GRAM_LAUNCH(32, 4, 2, 2, 2, 2);
         else GRAM_LAUNCH(32, 4, 2, 2, 4, 1);

@@ -1,0 +1,205 @@
+// Device-side m x m factorizations and iteration bookkeeping shared by the
+// single-CTA kernels (small.cu) and the fused kernels' last-CTA epilogues
+// (fused.cu).  All functions are called by every thread of one CTA.
+//
+// Cholesky follows the row-oriented form of cholesky_small (linalg.py:164-184):
+//   piv_j = B_jj - R[:j,j].R[:j,j];  breakdown if !finite(piv) or piv <= tol*max|diag B|
+//   R_jj = sqrt(piv);  R[j,k] = (B_jk - R[:j,j].R[:j,k]) / R_jj   (k > j)
+// and the triangular solves of trsm_right_inv (linalg.py:187-196) become a
+// multiply by the explicit upper inverse S = R^-1.
+#pragma once
+#include <math.h>
+#include "common.cuh"
+
+namespace ekcg_dev {
+
+constexpr int kMaxM = 64;
+
+
+// Cholesky of the symmetric m x m matrix in smem B (row-major); R (smem) gets
+// the upper factor.  Returns -1 on success, else the failing column (and the
+// pivot/scale through the references).  All threads participate.
+__device__ inline int chol_rows(const double* B, double* R, int m, double tol, double& piv_out,
+                         double& scale_out) {
+    __shared__ double s_piv;
+    __shared__ int s_fail;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < m * m; e += blockDim.x) R[e] = 0.0;
+    if (tid == 0) {
+        double sc = 0.0;
+        for (int j = 0; j < m; ++j) sc = fmax(sc, fabs(B[j * m + j]));
+        scale_out = sc;
+        s_fail = -1;
+    }
+    __syncthreads();
+    const double scale = scale_out;
+    for (int j = 0; j < m; ++j) {
+        if (tid == 0) {
+            double dot = 0.0;
+            for (int i = 0; i < j; ++i) dot += R[i * m + j] * R[i * m + j];
+            double piv = B[j * m + j] - dot;
+            if (!isfinite(piv) || piv <= tol * scale) {
+                s_fail = j;
+                s_piv = piv;
+            } else {
+                R[j * m + j] = sqrt(piv);
+            }
+        }
+        __syncthreads();
+        if (s_fail >= 0) {
+            piv_out = s_piv;
+            return s_fail;
+        }
+        const double rjj = R[j * m + j];
+        for (int k = j + 1 + tid; k < m; k += blockDim.x) {
+            double dot = 0.0;
+            for (int i = 0; i < j; ++i) dot += R[i * m + j] * R[i * m + k];
+            R[j * m + k] = (B[j * m + k] - dot) / rjj;
+        }
+        __syncthreads();
+    }
+    return -1;
+}
+
+// S = R^-1 for upper-triangular R: one thread per column, back substitution.
+__device__ inline void tri_inverse(const double* R, double* S, int m) {
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = 0.0;
+    __syncthreads();
+    for (int c = threadIdx.x; c < m; c += blockDim.x) {
+        S[c * m + c] = 1.0 / R[c * m + c];
+        for (int i = c - 1; i >= 0; --i) {
+            double s = 0.0;
+            for (int k = i + 1; k <= c; ++k) s += R[i * m + k] * S[k * m + c];
+            S[i * m + c] = -s / R[i * m + i];
+        }
+    }
+    __syncthreads();
+}
+
+__device__ inline void record_breakdown(EkcgCtrl* ctrl, int kind, int col, double piv, double scale, int iteration) {
+    ctrl->brk_kind = kind;
+    ctrl->brk_col = col;
+    ctrl->brk_pivot = piv;
+    ctrl->brk_scale = scale;
+    ctrl->brk_iter = iteration;
+    ctrl->status = 3;
+    ctrl->live = 0;
+}
+
+
+// Pre-CholQR factor from the raw Gram G = W^T W (smem, m x m, overwritten):
+// column norms D (aortho.py:74-79), G0 = sym(D^-1 G D^-1), R0 = chol(G0),
+// S0 = D^-1 R0^-1 written to global S0out.  R, S: smem scratch (m*m each).
+__device__ inline void prechol_body(double* G, double* R, double* S, int m, double* S0out, EkcgCtrl* ctrl,
+                                    int iteration, double tol) {
+    __shared__ double nrm[kMaxM];
+    __shared__ int dead;
+    __shared__ double piv, scale;
+    const int tid = threadIdx.x;
+    if (tid == 0) dead = -1;
+    for (int j = tid; j < m; j += blockDim.x) nrm[j] = sqrt(G[j * m + j]);
+    __syncthreads();
+    if (tid == 0) {
+        for (int j = 0; j < m; ++j)
+            if (nrm[j] == 0.0) { dead = j; break; }
+        if (dead >= 0) record_breakdown(ctrl, 1, dead, 0.0, 0.0, iteration);
+    }
+    __syncthreads();
+    if (dead >= 0) return;
+    // G0 = sym(D^-1 G D^-1) into R (as scratch), then back into G
+    for (int e = tid; e < m * m; e += blockDim.x) {
+        int a = e / m, b = e % m;
+        double gab = G[a * m + b] / nrm[a] / nrm[b];
+        double gba = G[b * m + a] / nrm[b] / nrm[a];
+        R[e] = 0.5 * (gab + gba);
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += blockDim.x) G[e] = R[e];
+    __syncthreads();
+    int fail = chol_rows(G, R, m, tol, piv, scale);
+    if (fail >= 0) {
+        if (tid == 0) record_breakdown(ctrl, 2, fail, piv, scale, iteration);
+        return;
+    }
+    tri_inverse(R, S, m);
+    for (int e = tid; e < m * m; e += blockDim.x) S0out[e] = S[e] / nrm[e / m];
+}
+
+// A-CholQR factor: R = chol(sym(G)), S = R^-1 written to global Sout.  G
+// (smem, m x m) is overwritten.
+__device__ inline void cholinv_body(double* G, double* R, double* S, int m, double* Sout, EkcgCtrl* ctrl,
+                                    int iteration, double tol) {
+    __shared__ double piv, scale;
+    const int tid = threadIdx.x;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+        int a = e / m, b = e % m;
+        R[e] = 0.5 * (G[a * m + b] + G[b * m + a]);
+    }
+    __syncthreads();
+    for (int e = tid; e < m * m; e += blockDim.x) G[e] = R[e];
+    __syncthreads();
+    int fail = chol_rows(G, R, m, tol, piv, scale);
+    if (fail >= 0) {
+        if (tid == 0) record_breakdown(ctrl, 2, fail, piv, scale, iteration);
+        return;
+    }
+    tri_inverse(R, S, m);
+    for (int e = tid; e < m * m; e += blockDim.x) Sout[e] = S[e];
+}
+
+// End of iteration k (solvers.py:398-415, :357), single thread.
+__device__ inline void finish_body(EkcgCtrl* ctrl, double rho2, int k, int kmax, int stagnation_window,
+                                   double* history) {
+    double rho = sqrt(rho2);
+    history[k] = rho;
+    ctrl->k_done = k;
+    ctrl->last_rho = rho;
+    if (rho < ctrl->best_rho) {
+        ctrl->best_rho = rho;
+        ctrl->best_k = k;
+    } else if (stagnation_window > 0 && k - ctrl->best_k >= stagnation_window) {
+        ctrl->status = 4;
+        ctrl->live = 0;
+        return;
+    }
+    if (!(rho > ctrl->tol_abs)) {
+        ctrl->status = 1;
+        ctrl->live = 0;
+    } else if (k + 1 > kmax) {
+        ctrl->status = 2;
+        ctrl->live = 0;
+    }
+}
+
+// "Last CTA" arrival for deterministic in-kernel reductions: every CTA has
+// written its partial; the CTA that increments the counter last returns true
+// (after a fence) and then sums all partials in fixed order.  It also resets
+// the counter for the next launch.
+__device__ inline bool last_cta_arrive(unsigned int* counter) {
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        unsigned total = gridDim.x * gridDim.y;
+        unsigned prev = atomicAdd(counter, 1u);
+        is_last = (prev == total - 1);
+        if (is_last) *counter = 0u;
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
+// out[j] = sum_{p < P} partials[p*len + j] (fixed order, L2-coherent loads), by one CTA.
+__device__ inline void cta_sum_partials(const double* partials, int P, int len, double* out) {
+    const int nthr = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (int j = tid; j < len; j += nthr) {
+        double s = __ldcg(partials + j);
+        for (int p = 1; p < P; ++p) s += __ldcg(partials + (long long)p * len + j);
+        out[j] = s;
+    }
+    __syncthreads();
+}
+
+}  // namespace ekcg_dev

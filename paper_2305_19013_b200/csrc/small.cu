@@ -12,144 +12,33 @@
 
 unsigned long long g_ekcg_launches = 0;
 
+#include "factor.cuh"
+
 namespace {
 
+using namespace ekcg_dev;
 constexpr int kSmallThreads = 256;
-constexpr int kMaxM = 64;
-
-// Cholesky of the symmetric m x m matrix in smem B (row-major); R (smem) gets
-// the upper factor.  Returns -1 on success, else the failing column (and the
-// pivot/scale through the references).  All threads participate.
-__device__ int chol_rows(const double* B, double* R, int m, double tol, double& piv_out,
-                         double& scale_out) {
-    __shared__ double s_piv;
-    __shared__ int s_fail;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < m * m; e += blockDim.x) R[e] = 0.0;
-    if (tid == 0) {
-        double sc = 0.0;
-        for (int j = 0; j < m; ++j) sc = fmax(sc, fabs(B[j * m + j]));
-        scale_out = sc;
-        s_fail = -1;
-    }
-    __syncthreads();
-    const double scale = scale_out;
-    for (int j = 0; j < m; ++j) {
-        if (tid == 0) {
-            double dot = 0.0;
-            for (int i = 0; i < j; ++i) dot += R[i * m + j] * R[i * m + j];
-            double piv = B[j * m + j] - dot;
-            if (!isfinite(piv) || piv <= tol * scale) {
-                s_fail = j;
-                s_piv = piv;
-            } else {
-                R[j * m + j] = sqrt(piv);
-            }
-        }
-        __syncthreads();
-        if (s_fail >= 0) {
-            piv_out = s_piv;
-            return s_fail;
-        }
-        const double rjj = R[j * m + j];
-        for (int k = j + 1 + tid; k < m; k += blockDim.x) {
-            double dot = 0.0;
-            for (int i = 0; i < j; ++i) dot += R[i * m + j] * R[i * m + k];
-            R[j * m + k] = (B[j * m + k] - dot) / rjj;
-        }
-        __syncthreads();
-    }
-    return -1;
-}
-
-// S = R^-1 for upper-triangular R: one thread per column, back substitution.
-__device__ void tri_inverse(const double* R, double* S, int m) {
-    for (int e = threadIdx.x; e < m * m; e += blockDim.x) S[e] = 0.0;
-    __syncthreads();
-    for (int c = threadIdx.x; c < m; c += blockDim.x) {
-        S[c * m + c] = 1.0 / R[c * m + c];
-        for (int i = c - 1; i >= 0; --i) {
-            double s = 0.0;
-            for (int k = i + 1; k <= c; ++k) s += R[i * m + k] * S[k * m + c];
-            S[i * m + c] = -s / R[i * m + i];
-        }
-    }
-    __syncthreads();
-}
-
-__device__ void record_breakdown(EkcgCtrl* ctrl, int kind, int col, double piv, double scale, int iteration) {
-    ctrl->brk_kind = kind;
-    ctrl->brk_col = col;
-    ctrl->brk_pivot = piv;
-    ctrl->brk_scale = scale;
-    ctrl->brk_iter = iteration;
-    ctrl->status = 3;
-    ctrl->live = 0;
-}
 
 __global__ void __launch_bounds__(kSmallThreads)
 prechol_kernel(const double* __restrict__ Graw, int m, double* __restrict__ S0, EkcgCtrl* ctrl,
                int iteration, double tol) {
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
-    double* B = sm;
-    double* R = B + m * m;
-    double* S = R + m * m;
-    __shared__ double nrm[kMaxM];
-    __shared__ int dead;
-    __shared__ double piv, scale;
-    const int tid = threadIdx.x;
-    if (tid == 0) dead = -1;
+    double* G = sm;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) G[e] = Graw[e];
     __syncthreads();
-    // column norms (aortho.py:74-79): a zero column is a breakdown
-    for (int j = tid; j < m; j += blockDim.x) nrm[j] = sqrt(Graw[j * m + j]);
-    __syncthreads();
-    if (tid == 0) {
-        for (int j = 0; j < m; ++j)
-            if (nrm[j] == 0.0) { dead = j; break; }
-        if (dead >= 0) record_breakdown(ctrl, 1, dead, 0.0, 0.0, iteration);
-    }
-    __syncthreads();
-    if (dead >= 0) return;
-    // G0 = sym(D^-1 Graw D^-1)  (aortho.py:21-22,105)
-    for (int e = tid; e < m * m; e += blockDim.x) {
-        int a = e / m, b = e % m;
-        double gab = Graw[a * m + b] / nrm[a] / nrm[b];
-        double gba = Graw[b * m + a] / nrm[b] / nrm[a];
-        B[e] = 0.5 * (gab + gba);
-    }
-    __syncthreads();
-    int fail = chol_rows(B, R, m, tol, piv, scale);
-    if (fail >= 0) {
-        if (tid == 0) record_breakdown(ctrl, 2, fail, piv, scale, iteration);
-        return;
-    }
-    tri_inverse(R, S, m);
-    for (int e = tid; e < m * m; e += blockDim.x) S0[e] = S[e] / nrm[e / m];
+    prechol_body(G, G + m * m, G + 2 * m * m, m, S0, ctrl, iteration, tol);
 }
 
 __global__ void __launch_bounds__(kSmallThreads)
-cholinv_kernel(const double* __restrict__ G, int m, double* __restrict__ Sout, EkcgCtrl* ctrl, int iteration,
+cholinv_kernel(const double* __restrict__ Gin, int m, double* __restrict__ Sout, EkcgCtrl* ctrl, int iteration,
                double tol) {
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
-    double* B = sm;
-    double* R = B + m * m;
-    double* S = R + m * m;
-    __shared__ double piv, scale;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < m * m; e += blockDim.x) {
-        int a = e / m, b = e % m;
-        B[e] = 0.5 * (G[a * m + b] + G[b * m + a]);
-    }
+    double* G = sm;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) G[e] = Gin[e];
     __syncthreads();
-    int fail = chol_rows(B, R, m, tol, piv, scale);
-    if (fail >= 0) {
-        if (tid == 0) record_breakdown(ctrl, 2, fail, piv, scale, iteration);
-        return;
-    }
-    tri_inverse(R, S, m);
-    for (int e = tid; e < m * m; e += blockDim.x) Sout[e] = S[e];
+    cholinv_body(G, G + m * m, G + 2 * m * m, m, Sout, ctrl, iteration, tol);
 }
 
 __global__ void __launch_bounds__(kSmallThreads)
@@ -199,25 +88,7 @@ __global__ void start_kernel(EkcgCtrl* ctrl, const double* __restrict__ rho2, do
 __global__ void finish_kernel(EkcgCtrl* ctrl, const double* __restrict__ rho2, int k, int kmax,
                               int stagnation_window, double* __restrict__ history) {
     if (ctrl->live == 0) return;
-    double rho = sqrt(*rho2);
-    history[k] = rho;
-    ctrl->k_done = k;
-    ctrl->last_rho = rho;
-    if (rho < ctrl->best_rho) {
-        ctrl->best_rho = rho;
-        ctrl->best_k = k;
-    } else if (stagnation_window > 0 && k - ctrl->best_k >= stagnation_window) {
-        ctrl->status = 4;
-        ctrl->live = 0;
-        return;
-    }
-    if (!(rho > ctrl->tol_abs)) {
-        ctrl->status = 1;
-        ctrl->live = 0;
-    } else if (k + 1 > kmax) {
-        ctrl->status = 2;
-        ctrl->live = 0;
-    }
+    finish_body(ctrl, *rho2, k, kmax, stagnation_window, history);
 }
 
 __global__ void store_norm_kernel(const double* __restrict__ rho2, double* __restrict__ checks, int slot,

@@ -9,6 +9,7 @@
 // reproduce that association with __dmul_rn/__dadd_rn (no FMA contraction).
 #include "common.cuh"
 #include "ekcg_b200.h"
+#include "stencil.cuh"
 
 // ---------------------------------------------------------------------------
 // Launch shape shared by the row-wise kernels: blockDim = (G, R) with G threads
@@ -145,123 +146,26 @@ __global__ void csr_spmm_kernel(const long long* __restrict__ rp, const int* __r
 // of the np.add.at calls in generators.py:46-53.  Row entries in column order:
 // z-, y-, x-, diag, x+, y+, z+.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ double harmonic_face(double c, double klo, double khi) {
-    // generators.py:45 -- `2.0 * ka * kb / (ka + kb)` evaluated left to right.
-    double h = __ddiv_rn(mul_rn(mul_rn(2.0, klo), khi), add_rn(klo, khi));
-    return mul_rn(c, h);
-}
-
-// Per-launch constants for a uniform-kappa grid: faces and boundary terms per
-// axis are the same everywhere, computed once on the device by the first
-// thread that needs them would cost a barrier; the host passes them instead
-// (same IEEE operations, so the same bits as harmonic_face()).
-struct UniformFaces {
-    double fz, fy, fx;  // c * 2k^2/(2k)
-    double bz, by, bx;  // c * k
-};
-
 template <int VEC>
 __global__ void __launch_bounds__(256)
 stencil_spmm_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X, int ldx,
                     double* __restrict__ Y, int ldy, int m, const int* __restrict__ live) {
     EKCG_GATE(live);
-    const unsigned nx = s.nx, ny = s.ny, nz = s.nz;
-    const long long nxy = (long long)nx * ny;
-    const long long n = nxy * nz;
-    const bool three = (s.dim == 3);
-    const bool uniform = (s.kfield == nullptr);
+    const long long n = (long long)s.nx * s.ny * s.nz;
     const int c0 = threadIdx.x * VEC;
     ROW_LOOP(i, n) {
-        const unsigned iu = (unsigned)i;
-        const unsigned x = iu % nx;
-        const unsigned rest = iu / nx;
-        const unsigned y = rest % ny;
-        const unsigned z = rest / ny;
-
-        double fzl = 0.0, fzh = 0.0, fyl = 0.0, fyh = 0.0, fxl = 0.0, fxh = 0.0;
-        double diag = 0.0;
-        if (uniform) {
-            if (three) {
-                if (z < nz - 1) { fzh = uf.fz; diag = add_rn(diag, fzh); }
-                if (z > 0)      { fzl = uf.fz; diag = add_rn(diag, fzl); }
-                if (z == 0)      diag = add_rn(diag, uf.bz);
-                if (z == nz - 1) diag = add_rn(diag, uf.bz);
-            }
-            if (y < ny - 1) { fyh = uf.fy; diag = add_rn(diag, fyh); }
-            if (y > 0)      { fyl = uf.fy; diag = add_rn(diag, fyl); }
-            if (y == 0)      diag = add_rn(diag, uf.by);
-            if (y == ny - 1) diag = add_rn(diag, uf.by);
-            if (x < nx - 1) { fxh = uf.fx; diag = add_rn(diag, fxh); }
-            if (x > 0)      { fxl = uf.fx; diag = add_rn(diag, fxl); }
-            if (x == 0)      diag = add_rn(diag, uf.bx);
-            if (x == nx - 1) diag = add_rn(diag, uf.bx);
-        } else {
-            // tile coordinates of the node; a neighbour is in the adjacent tile
-            // exactly when the step crosses a tile edge
-            const unsigned txi = x / (unsigned)s.tx, tyi = y / (unsigned)s.ty, tzi = z / (unsigned)s.tz;
-            const unsigned rx = x - txi * s.tx, ry = y - tyi * s.ty, rz = z - tzi * s.tz;
-            const long long fx = s.fx, fxy = (long long)s.fx * s.fy;
-            const double* __restrict__ F = s.kfield;
-            const long long tc = tzi * fxy + tyi * fx + txi;
-            const double kc = F[tc];
-            if (three) {
-                if (z < nz - 1) { fzh = harmonic_face(s.cz, kc, F[tc + (rz + 1 == (unsigned)s.tz ? fxy : 0)]); diag = add_rn(diag, fzh); }
-                if (z > 0)      { fzl = harmonic_face(s.cz, F[tc - (rz == 0 ? fxy : 0)], kc); diag = add_rn(diag, fzl); }
-                if (z == 0)      diag = add_rn(diag, mul_rn(s.cz, kc));
-                if (z == nz - 1) diag = add_rn(diag, mul_rn(s.cz, kc));
-            }
-            if (y < ny - 1) { fyh = harmonic_face(s.cy, kc, F[tc + (ry + 1 == (unsigned)s.ty ? fx : 0)]); diag = add_rn(diag, fyh); }
-            if (y > 0)      { fyl = harmonic_face(s.cy, F[tc - (ry == 0 ? fx : 0)], kc); diag = add_rn(diag, fyl); }
-            if (y == 0)      diag = add_rn(diag, mul_rn(s.cy, kc));
-            if (y == ny - 1) diag = add_rn(diag, mul_rn(s.cy, kc));
-            if (x < nx - 1) { fxh = harmonic_face(s.cx, kc, F[tc + (rx + 1 == (unsigned)s.tx ? 1 : 0)]); diag = add_rn(diag, fxh); }
-            if (x > 0)      { fxl = harmonic_face(s.cx, F[tc - (rx == 0 ? 1 : 0)], kc); diag = add_rn(diag, fxl); }
-            if (x == 0)      diag = add_rn(diag, mul_rn(s.cx, kc));
-            if (x == nx - 1) diag = add_rn(diag, mul_rn(s.cx, kc));
-        }
-
-        // row entries in ascending column order: z-, y-, x-, diag, x+, y+, z+
         long long off[7];
         double val[7];
-        int cnt = 0;
-        if (three && z > 0)      { off[cnt] = i - nxy; val[cnt++] = -fzl; }
-        if (y > 0)               { off[cnt] = i - nx;  val[cnt++] = -fyl; }
-        if (x > 0)               { off[cnt] = i - 1;   val[cnt++] = -fxl; }
-        off[cnt] = i; val[cnt++] = diag;
-        if (x < nx - 1)          { off[cnt] = i + 1;   val[cnt++] = -fxh; }
-        if (y < ny - 1)          { off[cnt] = i + nx;  val[cnt++] = -fyh; }
-        if (three && z < nz - 1) { off[cnt] = i + nxy; val[cnt++] = -fzh; }
-
+        int dpos;
+        const int cnt = stencil_row(s, uf, i, off, val, dpos);
+        double y[VEC];
+        stencil_apply_row<VEC>(X, ldx, c0, m, off, val, cnt, y);
         if (VEC >= 2 && c0 + VEC <= m) {
-            // vector path: VEC/2 double2 loads per neighbour row (16 B aligned)
-            constexpr int H = VEC >= 2 ? VEC / 2 : 1;
-            double2 acc[H], p0[H];
-#pragma unroll
-            for (int h = 0; h < VEC / 2; ++h) {
-                double2 a = __ldg(reinterpret_cast<const double2*>(X + off[0] * ldx + c0) + h);
-                double2 b = __ldg(reinterpret_cast<const double2*>(X + off[1] * ldx + c0) + h);
-                p0[h] = make_double2(mul_rn(val[0], a.x), mul_rn(val[0], a.y));
-                acc[h] = make_double2(mul_rn(val[1], b.x), mul_rn(val[1], b.y));
-            }
-            for (int q = 2; q < cnt; ++q) {
-#pragma unroll
-                for (int h = 0; h < VEC / 2; ++h) {
-                    double2 a = __ldg(reinterpret_cast<const double2*>(X + off[q] * ldx + c0) + h);
-                    acc[h].x = add_rn(acc[h].x, mul_rn(val[q], a.x));
-                    acc[h].y = add_rn(acc[h].y, mul_rn(val[q], a.y));
-                }
-            }
 #pragma unroll
             for (int h = 0; h < VEC / 2; ++h)
-                reinterpret_cast<double2*>(Y + i * ldy + c0)[h] =
-                    make_double2(add_rn(p0[h].x, acc[h].x), add_rn(p0[h].y, acc[h].y));
+                reinterpret_cast<double2*>(Y + i * ldy + c0)[h] = make_double2(y[2 * h], y[2 * h + 1]);
         } else {
-            for (int c = c0; c < c0 + VEC && c < m; ++c) {
-                double p0 = mul_rn(val[0], __ldg(X + off[0] * ldx + c));
-                double acc = mul_rn(val[1], __ldg(X + off[1] * ldx + c));
-                for (int q = 2; q < cnt; ++q) acc = add_rn(acc, mul_rn(val[q], __ldg(X + off[q] * ldx + c)));
-                Y[i * ldy + c] = add_rn(p0, acc);
-            }
+            for (int v = 0; v < VEC && c0 + v < m; ++v) Y[i * ldy + c0 + v] = y[v];
         }
     }
 }
@@ -269,14 +173,6 @@ stencil_spmm_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
-static double host_face(double c, double k) {
-    volatile double two_k = 2.0 * k;
-    volatile double num = two_k * k;
-    volatile double den = k + k;
-    volatile double h = num / den;
-    return c * h;
-}
-
 extern "C" int ekcg_split(const double* v, const int* owner, double* W, long long n, int t, int ldw,
                           const int* live, void* stream) {
     if (n < 0 || t < 1 || ldw < t) return EKCG_EINVAL;
@@ -313,23 +209,12 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
 
 extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
                                  int m, const int* live, void* stream) {
-    if (desc == nullptr || m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
-    EkcgStencil s = *desc;
-    if (s.dim != 2 && s.dim != 3) return EKCG_EINVAL;
-    if (s.dim == 2) s.nz = 1;
-    if (s.nx < 2 || s.ny < 2 || (s.dim == 3 && s.nz < 2)) return EKCG_EINVAL;
-    if (s.kfield != nullptr && (s.tx < 1 || s.ty < 1 || s.tz < 1 || s.fx < 1 || s.fy < 1)) return EKCG_EINVAL;
-    long long n = (long long)s.nx * s.ny * s.nz;
-    if (n >= (1LL << 32)) return EKCG_EINVAL;
-    UniformFaces uf{};
-    if (s.kfield == nullptr) {
-        uf.fz = host_face(s.cz, s.kconst);
-        uf.fy = host_face(s.cy, s.kconst);
-        uf.fx = host_face(s.cx, s.kconst);
-        uf.bz = s.cz * s.kconst;
-        uf.by = s.cy * s.kconst;
-        uf.bx = s.cx * s.kconst;
-    }
+    if (m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
+    EkcgStencil s;
+    UniformFaces uf;
+    long long n;
+    int rc = prepare_stencil(desc, s, uf, n);
+    if (rc != EKCG_OK) return rc;
     cudaStream_t st = as_stream(stream);
     const bool aligned = (ldx % 2 == 0) && (ldy % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);

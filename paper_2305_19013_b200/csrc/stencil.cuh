@@ -1,0 +1,167 @@
+// Structured-grid stencil rows (the `_diffusion_matrix` operator of
+// generators.py:25-60) shared by the plain and fused stencil kernels.
+//
+// Face between lo/hi nodes: c * (2*k_lo*k_hi/(k_lo+k_hi)); Dirichlet boundary
+// faces add c * k_node.  The diagonal accumulates, per axis from slowest to
+// fastest: +face_hi, +face_lo, +boundary(first), +boundary(last) -- the order
+// of the np.add.at calls in generators.py:46-53.  Row entries come out in
+// ascending column order (z-, y-, x-, diag, x+, y+, z+) and a row is summed as
+// p0 + (((p1 + p2) + p3) + ...) with separately rounded products: bitwise the
+// reference spmm on the assembled CSR (linalg.py:141-152).
+#pragma once
+#include "common.cuh"
+#include "ekcg_b200.h"
+
+__device__ __forceinline__ double harmonic_face(double c, double klo, double khi) {
+    // generators.py:45 -- `2.0 * ka * kb / (ka + kb)` evaluated left to right.
+    double h = __ddiv_rn(mul_rn(mul_rn(2.0, klo), khi), add_rn(klo, khi));
+    return mul_rn(c, h);
+}
+
+// Per-launch constants for a uniform-kappa grid (computed by the host with the
+// same IEEE operations as harmonic_face, so the same bits).
+struct UniformFaces {
+    double fz, fy, fx;  // c * 2k^2/(2k)
+    double bz, by, bx;  // c * k
+};
+
+// Row i of the operator: neighbour offsets and values in column order.
+// Returns the entry count; `dpos` gets the position of the diagonal entry.
+__device__ __forceinline__ int stencil_row(const EkcgStencil& s, const UniformFaces& uf, long long i,
+                                           long long (&off)[7], double (&val)[7], int& dpos) {
+    const unsigned nx = s.nx, ny = s.ny, nz = s.nz;
+    const long long nxy = (long long)nx * ny;
+    const bool three = (s.dim == 3);
+    const unsigned iu = (unsigned)i;
+    const unsigned x = iu % nx;
+    const unsigned rest = iu / nx;
+    const unsigned y = rest % ny;
+    const unsigned z = rest / ny;
+
+    double fzl = 0.0, fzh = 0.0, fyl = 0.0, fyh = 0.0, fxl = 0.0, fxh = 0.0;
+    double diag = 0.0;
+    if (s.kfield == nullptr) {
+        if (three) {
+            if (z < nz - 1) { fzh = uf.fz; diag = add_rn(diag, fzh); }
+            if (z > 0)      { fzl = uf.fz; diag = add_rn(diag, fzl); }
+            if (z == 0)      diag = add_rn(diag, uf.bz);
+            if (z == nz - 1) diag = add_rn(diag, uf.bz);
+        }
+        if (y < ny - 1) { fyh = uf.fy; diag = add_rn(diag, fyh); }
+        if (y > 0)      { fyl = uf.fy; diag = add_rn(diag, fyl); }
+        if (y == 0)      diag = add_rn(diag, uf.by);
+        if (y == ny - 1) diag = add_rn(diag, uf.by);
+        if (x < nx - 1) { fxh = uf.fx; diag = add_rn(diag, fxh); }
+        if (x > 0)      { fxl = uf.fx; diag = add_rn(diag, fxl); }
+        if (x == 0)      diag = add_rn(diag, uf.bx);
+        if (x == nx - 1) diag = add_rn(diag, uf.bx);
+    } else {
+        // tile coordinates of the node; a neighbour lies in the adjacent tile
+        // exactly when the step crosses a tile edge
+        const unsigned txi = x / (unsigned)s.tx, tyi = y / (unsigned)s.ty, tzi = z / (unsigned)s.tz;
+        const unsigned rx = x - txi * s.tx, ry = y - tyi * s.ty, rz = z - tzi * s.tz;
+        const long long fx = s.fx, fxy = (long long)s.fx * s.fy;
+        const double* __restrict__ F = s.kfield;
+        const long long tc = tzi * fxy + tyi * fx + txi;
+        const double kc = __ldg(F + tc);
+        if (three) {
+            if (z < nz - 1) { fzh = harmonic_face(s.cz, kc, __ldg(F + tc + (rz + 1 == (unsigned)s.tz ? fxy : 0))); diag = add_rn(diag, fzh); }
+            if (z > 0)      { fzl = harmonic_face(s.cz, __ldg(F + tc - (rz == 0 ? fxy : 0)), kc); diag = add_rn(diag, fzl); }
+            if (z == 0)      diag = add_rn(diag, mul_rn(s.cz, kc));
+            if (z == nz - 1) diag = add_rn(diag, mul_rn(s.cz, kc));
+        }
+        if (y < ny - 1) { fyh = harmonic_face(s.cy, kc, __ldg(F + tc + (ry + 1 == (unsigned)s.ty ? fx : 0))); diag = add_rn(diag, fyh); }
+        if (y > 0)      { fyl = harmonic_face(s.cy, __ldg(F + tc - (ry == 0 ? fx : 0)), kc); diag = add_rn(diag, fyl); }
+        if (y == 0)      diag = add_rn(diag, mul_rn(s.cy, kc));
+        if (y == ny - 1) diag = add_rn(diag, mul_rn(s.cy, kc));
+        if (x < nx - 1) { fxh = harmonic_face(s.cx, kc, __ldg(F + tc + (rx + 1 == (unsigned)s.tx ? 1 : 0))); diag = add_rn(diag, fxh); }
+        if (x > 0)      { fxl = harmonic_face(s.cx, __ldg(F + tc - (rx == 0 ? 1 : 0)), kc); diag = add_rn(diag, fxl); }
+        if (x == 0)      diag = add_rn(diag, mul_rn(s.cx, kc));
+        if (x == nx - 1) diag = add_rn(diag, mul_rn(s.cx, kc));
+    }
+
+    int cnt = 0;
+    if (three && z > 0)      { off[cnt] = i - nxy; val[cnt++] = -fzl; }
+    if (y > 0)               { off[cnt] = i - nx;  val[cnt++] = -fyl; }
+    if (x > 0)               { off[cnt] = i - 1;   val[cnt++] = -fxl; }
+    dpos = cnt;
+    off[cnt] = i; val[cnt++] = diag;
+    if (x < nx - 1)          { off[cnt] = i + 1;   val[cnt++] = -fxh; }
+    if (y < ny - 1)          { off[cnt] = i + nx;  val[cnt++] = -fyh; }
+    if (three && z < nz - 1) { off[cnt] = i + nxy; val[cnt++] = -fzh; }
+    return cnt;
+}
+
+// y[c0 .. c0+VEC) of row i (VEC even and 16-B aligned rows use double2 loads).
+template <int VEC>
+__device__ __forceinline__ void stencil_apply_row(const double* __restrict__ X, int ldx, int c0, int m,
+                                                  const long long (&off)[7], const double (&val)[7], int cnt,
+                                                  double (&y)[VEC]) {
+    if (VEC >= 2 && c0 + VEC <= m) {
+        constexpr int H = VEC >= 2 ? VEC / 2 : 1;
+        double2 acc[H], p0[H];
+#pragma unroll
+        for (int h = 0; h < VEC / 2; ++h) {
+            double2 a = __ldg(reinterpret_cast<const double2*>(X + off[0] * ldx + c0) + h);
+            double2 b = __ldg(reinterpret_cast<const double2*>(X + off[1] * ldx + c0) + h);
+            p0[h] = make_double2(mul_rn(val[0], a.x), mul_rn(val[0], a.y));
+            acc[h] = make_double2(mul_rn(val[1], b.x), mul_rn(val[1], b.y));
+        }
+        for (int q = 2; q < cnt; ++q) {
+#pragma unroll
+            for (int h = 0; h < VEC / 2; ++h) {
+                double2 a = __ldg(reinterpret_cast<const double2*>(X + off[q] * ldx + c0) + h);
+                acc[h].x = add_rn(acc[h].x, mul_rn(val[q], a.x));
+                acc[h].y = add_rn(acc[h].y, mul_rn(val[q], a.y));
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < VEC / 2; ++h) {
+            y[2 * h] = add_rn(p0[h].x, acc[h].x);
+            y[2 * h + 1] = add_rn(p0[h].y, acc[h].y);
+        }
+    } else {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) {
+            const int c = c0 + v;
+            if (c >= m) {
+                y[v] = 0.0;
+                continue;
+            }
+            double p0 = mul_rn(val[0], __ldg(X + off[0] * ldx + c));
+            double acc = mul_rn(val[1], __ldg(X + off[1] * ldx + c));
+            for (int q = 2; q < cnt; ++q) acc = add_rn(acc, mul_rn(val[q], __ldg(X + off[q] * ldx + c)));
+            y[v] = add_rn(p0, acc);
+        }
+    }
+}
+
+static inline double host_face(double c, double k) {
+    volatile double two_k = 2.0 * k;
+    volatile double num = two_k * k;
+    volatile double den = k + k;
+    volatile double h = num / den;
+    return c * h;
+}
+
+// Validate / normalise a descriptor and fill the uniform-face constants.
+static inline int prepare_stencil(const EkcgStencil* desc, EkcgStencil& s, UniformFaces& uf, long long& n) {
+    if (desc == nullptr) return EKCG_EINVAL;
+    s = *desc;
+    if (s.dim != 2 && s.dim != 3) return EKCG_EINVAL;
+    if (s.dim == 2) s.nz = 1;
+    if (s.nx < 2 || s.ny < 2 || (s.dim == 3 && s.nz < 2)) return EKCG_EINVAL;
+    if (s.kfield != nullptr && (s.tx < 1 || s.ty < 1 || s.tz < 1 || s.fx < 1 || s.fy < 1)) return EKCG_EINVAL;
+    n = (long long)s.nx * s.ny * s.nz;
+    if (n >= (1LL << 32)) return EKCG_EINVAL;
+    uf = UniformFaces{};
+    if (s.kfield == nullptr) {
+        uf.fz = host_face(s.cz, s.kconst);
+        uf.fy = host_face(s.cy, s.kconst);
+        uf.fx = host_face(s.cx, s.kconst);
+        uf.bz = s.cz * s.kconst;
+        uf.by = s.cy * s.kconst;
+        uf.bx = s.cx * s.kconst;
+    }
+    return EKCG_OK;
+}

@@ -94,6 +94,10 @@ class DeviceEngine:
         self.sync_mode = False
         self.max_lookahead = 16
         self.kernel_timer = None  # optional hook: (name, callable) -> runs callable
+        self.no_fuse = False      # force the unfused kernel sequence (tests / A-B timing)
+        # fused stages in use when the operator/width allow: "prechol" (update2 + Graw + S0),
+        # "cholinv" (A W0 + G + S), "vec" (W0 S + alpha), "xr" (A W_k + x/r + finish)
+        self.fuse = {"cholinv", "vec", "xr"}
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -137,6 +141,10 @@ class DeviceEngine:
         self.switch_iteration = None
         self.gram_chunks = {}
         self.launch_k = []
+        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        from .operators import StencilOperator
+        self.fused_ok = isinstance(self.op, StencilOperator) and not self.no_fuse
+        self.fused_part = _lib.query("ekcg_fused_partials", n, mm)
 
     def _ensure(self, name, numel):
         buf = getattr(self, name)
@@ -271,15 +279,27 @@ class DeviceEngine:
             _lib.call("ekcg_split_axpy", self.r.data_ptr(), self.owner_dev.data_ptr(), newest.q.data_ptr(),
                       newest.width, self.beta.data_ptr(), -1.0, WA, n, t, m, live, st)
 
+        fused = (self.fused_ok and m in (8, 16, 32, 64)
+                 and all(b.width == m for b in self.retained))
+        if fused:
+            part = self._ensure("part", self.fused_part)
         # ---- CGS2 against the retained history (aortho.py:89-95) ----
+        have_s0 = False
         if d > 0:
             csz = sum((e - s0) * wg * m for s0, e, wg in groups)
             C = self._ensure("C", csz)
-            for _ in range(2):
+            for pas in range(2):
                 off = 0
                 for s0, e, wg in groups:  # all coefficients from the same W (classical GS)
                     self._gram(aq_addr(s0), wg, e - s0, wg, W, m, m, C.data_ptr() + F64 * off, tag="hist_gram")
                     off += (e - s0) * wg * m
+                if fused and pas == 1 and "prechol" in self.fuse:
+                    # W'' = W' - Q C2 fused with Graw = W''^T W'' and the Pre-CholQR factor
+                    self._timed("hist_update", lambda: _lib.call(
+                        "ekcg_update_prechol", q_addr(0), m, d, C.data_ptr(), WA, m, WA, m, m, n,
+                        part.data_ptr(), self.counter.data_ptr(), self.S0.data_ptr(), live, k, 1e-14, st))
+                    have_s0 = True
+                    break
                 off = 0
                 win = W
                 for s0, e, wg in groups:
@@ -290,31 +310,55 @@ class DeviceEngine:
                 W = WA
 
         # ---- Pre-CholQR (aortho.py:98-110) ----
-        self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
-        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+        if not have_s0:
+            self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
+            _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
         self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WB, m, m, 0.0, 1.0, tag="tri_apply")
-        self._apply_op(WB, m, WC, m, m)
-        self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_self")
-        _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
-        self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
-                     tag="tri_apply")
-        self._apply_op(blk.q.data_ptr(), m, blk.aq.data_ptr(), m, m)
+        finish_now = (k % self.every != 0)
+        if fused and "cholinv" in self.fuse:
+            # G = W0^T A W0 (A W0 never written) + A-CholQR factor S
+            self._timed("spmm_gram", lambda: _lib.call(
+                "ekcg_stencil_cholinv", self.op.desc_ref(), WB, m, m, part.data_ptr(), self.counter.data_ptr(),
+                self.S.data_ptr(), live, k, 1e-14, st))
+        else:
+            self._apply_op(WB, m, WC, m, m)
+            self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_self")
+            _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+        if fused and "vec" in self.fuse:
+            # W_k = W0 S + alpha = W_k^T r
+            self._timed("tri_alpha", lambda: _lib.call(
+                "ekcg_update_vec", WB_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
+                part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
+        else:
+            self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
+                         tag="tri_apply")
+            self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
+        xr_fused = fused and "xr" in self.fuse
+        if xr_fused:
+            # AW_k = A W_k + x/r update + |r|^2 + end-of-iteration bookkeeping (solvers.py:394-415)
+            self._ensure_history(k + 1)
+            self._timed("spmm_xr", lambda: _lib.call(
+                "ekcg_stencil_xr", self.op.desc_ref(), blk.q.data_ptr(), m, blk.aq.data_ptr(), m, m,
+                self.alpha.data_ptr(), self.x.data_ptr(), self.r.data_ptr(), part.data_ptr(),
+                self.counter.data_ptr(), live, k, self.kmax, self.stag_window, self.history.data_ptr(),
+                1 if finish_now else 0, self.rho2.data_ptr(), st))
+        else:
+            self._apply_op(blk.q.data_ptr(), m, blk.aq.data_ptr(), m, m)
+            # ---- iterate update (solvers.py:394-399) ----
+            self._timed("xr_update", lambda: _lib.call(
+                "ekcg_xr_update", blk.q.data_ptr(), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
+                self.x.data_ptr(), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st))
+            _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
         self._append(blk)
-
-        # ---- iterate update (solvers.py:394-399) ----
-        self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
-        self._timed("xr_update", lambda: _lib.call(
-            "ekcg_xr_update", blk.q.data_ptr(), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
-            self.x.data_ptr(), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st))
-        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
-        if k % self.every == 0:  # true-residual drift log (solvers.py:401-402)
+        if not finish_now:  # true-residual drift log (solvers.py:401-402)
             slot = k // self.every - 1
             self._ensure_checks(slot + 1)
             self._residual_sq(self.x, self.tr2, live)
             _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
-        self._ensure_history(k + 1)
-        _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
-                  self.history.data_ptr(), st)
+        if not (xr_fused and finish_now):
+            self._ensure_history(k + 1)
+            _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+                      self.history.data_ptr(), st)
         self._account(k, d, m, fresh, t)
 
     def _chain(self, V, m, t):

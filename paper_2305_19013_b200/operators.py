@@ -127,6 +127,9 @@ class StencilOperator:
         from .problems import diffusion_csr
         return diffusion_csr(self.shape, self.node_kappa(), self.axis_coef)
 
+    def desc_ref(self):
+        return ctypes.byref(self._desc)
+
     def apply(self, X, ldx, Y, ldy, m, live=None, stream=None):
         st = current_stream_ptr(self.device) if stream is None else stream
         _lib.call("ekcg_spmm_stencil", ctypes.byref(self._desc), _ptr(X), ldx, _ptr(Y), ldy, m, live, st)

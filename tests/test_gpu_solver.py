@@ -235,3 +235,21 @@ def test_torch_io_stays_on_device():
     x, rep = pk.enlarged_solve(prob.stencil(), b, partition=prob.partition, cfg=SolverConfig(**prob.solver_kwargs))
     assert isinstance(x, torch.Tensor) and x.is_cuda
     assert rep.status == "converged"
+
+
+@pytest.mark.parametrize("idx,edge", [(2, 16), (3, 16), (5, 64), (4, 10), (1, 40)])
+def test_fused_matches_unfused(idx, edge):
+    """The fused stencil kernels (in-kernel reductions + factorizations) follow the
+    unfused kernel sequence to round-off on the same device."""
+    from paper_2305_19013_b200.engine import DeviceEngine
+    prob = make_config(idx, edge)
+    cfg = SolverConfig(**dict(prob.solver_kwargs, kmax=25))
+    op = prob.stencil()
+    reps = []
+    for no_fuse in (False, True):
+        eng = DeviceEngine(op, prob.partition, cfg)
+        eng.no_fuse = no_fuse
+        reps.append(eng.solve(prob.b)[1])
+    a, b = reps
+    assert a.iterations == b.iterations
+    assert hist_dev(a.residual_history, b.residual_history, k=10) <= 1e-9
