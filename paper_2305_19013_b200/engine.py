@@ -98,6 +98,11 @@ class DeviceEngine:
         # fused stages in use when the operator/width allow: "prechol" (update2 + Graw + S0),
         # "cholinv" (A W0 + G + S), "vec" (W0 S + alpha), "xr" (A W_k + x/r + finish)
         self.fuse = {"cholinv", "vec", "xr"}
+        # cache A Q next to every retained Q (reference scheme, aortho.py:82-87) or
+        # recompute the projections as Q^T (A W) with A symmetric ("lean": w + 2
+        # blocks of HBM instead of 2w + 3; two extra operator applications per
+        # iteration).  "auto" picks lean only when the cached scheme does not fit.
+        self.cache_aq = "auto"
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -107,8 +112,9 @@ class DeviceEngine:
         self.m_max = self.s * self.t_cur
         mm = self.m_max
         f64 = dict(dtype=torch.float64, device=dev)
+        self.lean = self._choose_lean(n, mm)
         self.WA = torch.empty(n * mm, **f64)
-        self.WB = torch.empty(n * mm, **f64)
+        self.WB = torch.empty(0 if self.lean else n * mm, **f64)
         self.WC = torch.empty(n * mm, **f64)
         self.tmpv = torch.empty(n, **f64)
         self.Graw = torch.empty(mm * mm, **f64)
@@ -145,6 +151,21 @@ class DeviceEngine:
         from .operators import StencilOperator
         self.fused_ok = isinstance(self.op, StencilOperator) and not self.no_fuse
         self.fused_part = _lib.query("ekcg_fused_partials", n, mm)
+
+    def _choose_lean(self, n, m):
+        eligible = (self.window is not None and self.s == 1 and self.method in ("sre-cg2", "sre-cg")
+                    and self.cfg.switch_tol is None)
+        if self.cache_aq is True or not eligible:
+            if self.cache_aq is False and not eligible:
+                raise ValueError("the lean (no A Q cache) scheme needs a truncation window, s = 1, "
+                                 "an SRE method and no flexible switch")
+            return False
+        if self.cache_aq is False:
+            return True
+        block = 8.0 * n * m
+        cached = (2 * self.window + 3) * block + 6 * 8.0 * n
+        free, _ = torch.cuda.mem_get_info(self.device)
+        return cached > 0.92 * free
 
     def _ensure(self, name, numel):
         buf = getattr(self, name)
@@ -194,7 +215,8 @@ class DeviceEngine:
             slot = self.since_clear % self.window
             if slot not in self.slots:
                 f64 = dict(dtype=torch.float64, device=self.device)
-                self.slots[slot] = (torch.empty(n * self.m_max, **f64), torch.empty(n * self.m_max, **f64))
+                aq = None if self.lean else torch.empty(n * self.m_max, **f64)
+                self.slots[slot] = (torch.empty(n * self.m_max, **f64), aq)
             qbuf, aqbuf = self.slots[slot]
         else:
             slot = -1
@@ -227,6 +249,8 @@ class DeviceEngine:
         return groups
 
     def _enqueue_iteration(self, k, tol1):
+        if self.lean:
+            return self._enqueue_iteration_lean(k, tol1)
         cfg, n = self.cfg, self.n
         st, live = self.stream, self.live
         # restart policies (solvers.py:358-364)
@@ -356,6 +380,85 @@ class DeviceEngine:
             self._residual_sq(self.x, self.tr2, live)
             _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
         if not (xr_fused and finish_now):
+            self._ensure_history(k + 1)
+            _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+                      self.history.data_ptr(), st)
+        self._account(k, d, m, fresh, t)
+
+    def _enqueue_iteration_lean(self, k, tol1):
+        """One iteration without cached A Q (HBM: w Q blocks + 2 scratch).
+
+        WA carries the candidate A W_{k-1} between iterations; the CGS2
+        coefficients are C = Q_i^T (A W) (A symmetric), so each pass applies the
+        operator once (into WC) instead of reading cached A Q_i.
+        """
+        cfg, n = self.cfg, self.n
+        st, live = self.stream, self.live
+        if k > 1 and self.retention == "restart" and k % cfg.restart_j == 1:
+            self._clear()
+            self.restarts.append(k)
+        elif (k > 1 and self.retention == "restart-tol" and tol1 < cfg.restart_tol
+              and (not self.restarts or k > self.restarts[-1] + 1)):
+            self._clear()
+            self.restarts.append(k)
+        t = self.t_cur
+        m = t
+        d = len(self.retained)
+        blk = self._new_block(m)
+        WA, WC = self.WA.data_ptr(), self.WC.data_ptr()
+        ptrs = [b.q.data_ptr() for b in self.retained] + [WA, WC, blk.q.data_ptr()]
+        base = self.arena.push(ptrs)
+        q_addr = lambda i: base + F64 * i
+        WA_arr, WC_arr, NEW_arr = (base + F64 * (d + j) for j in range(3))
+        fresh = not self.retained
+        if fresh:
+            _lib.call("ekcg_split", self.r.data_ptr(), self.owner_dev.data_ptr(), WA, n, t, m, live, st)
+        fused = self.fused_ok and m in (8, 16, 32, 64)
+        part = self._ensure("part", self.fused_part) if fused else None
+        if d > 0:
+            C = self._ensure("C", d * m * m)
+            for _ in range(2):
+                self._apply_op(WA, m, WC, m, m, tag="spmm_proj")
+                self._gram(q_addr(0), m, d, m, WC, m, m, C.data_ptr(), tag="hist_gram")
+                self._update(q_addr(0), m, d, m, C.data_ptr(), WA, m, WA, m, m, 1.0, -1.0, tag="hist_update")
+        self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
+        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+        self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WC, m, m, 0.0, 1.0, tag="tri_apply")  # W0 -> WC
+        if fused:
+            self._timed("spmm_gram", lambda: _lib.call(
+                "ekcg_stencil_cholinv", self.op.desc_ref(), WC, m, m, part.data_ptr(), self.counter.data_ptr(),
+                self.S.data_ptr(), live, k, 1e-14, st))
+            self._timed("tri_alpha", lambda: _lib.call(
+                "ekcg_update_vec", WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
+                part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
+        else:
+            self._apply_op(WC, m, WA, m, m)  # A W0 -> WA (free)
+            self._gram(WC_arr, m, 1, m, WA, m, m, self.G.data_ptr(), tag="gram_self")
+            _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+            self._update(WC_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
+                         tag="tri_apply")
+            self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
+        finish_now = (k % self.every != 0)
+        if fused:
+            self._ensure_history(k + 1)
+            self._timed("spmm_xr", lambda: _lib.call(
+                "ekcg_stencil_xr", self.op.desc_ref(), blk.q.data_ptr(), m, WA, m, m,
+                self.alpha.data_ptr(), self.x.data_ptr(), self.r.data_ptr(), part.data_ptr(),
+                self.counter.data_ptr(), live, k, self.kmax, self.stag_window, self.history.data_ptr(),
+                1 if finish_now else 0, self.rho2.data_ptr(), st))
+        else:
+            self._apply_op(blk.q.data_ptr(), m, WA, m, m)  # A W_k -> WA: next candidate
+            self._timed("xr_update", lambda: _lib.call(
+                "ekcg_xr_update", blk.q.data_ptr(), m, WA, m, self.alpha.data_ptr(), m,
+                self.x.data_ptr(), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st))
+            _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
+        self._append(blk)
+        if not finish_now:
+            slot = k // self.every - 1
+            self._ensure_checks(slot + 1)
+            self._residual_sq(self.x, self.tr2, live)
+            _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
+        if not (fused and finish_now):
             self._ensure_history(k + 1)
             _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
                       self.history.data_ptr(), st)
@@ -498,8 +601,15 @@ class DeviceEngine:
 
     def _state(self, k, rho, tol1, numpy_io):
         conv = (lambda t: t.cpu().numpy()) if numpy_io else (lambda t: t.clone())
-        blocks = [(b.q[: self.n * b.width].view(self.n, b.width), b.aq[: self.n * b.width].view(self.n, b.width))
-                  for b in self.retained]
+        blocks = []
+        for b in self.retained:
+            q = b.q[: self.n * b.width].view(self.n, b.width)
+            if b.aq is not None:
+                aq = b.aq[: self.n * b.width].view(self.n, b.width)
+            else:  # lean scheme: materialise A Q for the callback only
+                aq = torch.empty_like(q)
+                self._apply_op(q.data_ptr(), b.width, aq.data_ptr(), b.width, b.width, tag="spmm", live=None)
+            blocks.append((q, aq))
         return {"k": k, "x": conv(self.x), "r": conv(self.r), "rho": rho, "tol1": tol1,
                 "store": BasisStore(self.window, blocks, self.peak, to_host=numpy_io),
                 "partition": self.part_obj}
@@ -549,12 +659,18 @@ class DeviceEngine:
         return x_out, rep
 
     def _iter_bytes(self, d, m):
+        """8[(4d + 11) n m + 5 n] + 2 M_A, plus the s-step chain
+        (s - 1)(16 n t + M_A) when s > 1."""
         n = self.n
-        return 8.0 * ((4 * d + 11) * n * m + 5 * n) + 2 * self.op.matrix_bytes()
+        t = m // self.s
+        chain = (self.s - 1) * (16.0 * n * t + self.op.matrix_bytes())
+        return 8.0 * ((4 * d + 11) * n * m + 5 * n) + 2 * self.op.matrix_bytes() + chain
 
     def _iter_flops(self, d, m):
         n = self.n
-        return (8 * d + 6) * m * m * n + 4.0 * self._nnz() * m + 6.0 * m * n
+        t = m // self.s
+        chain = (self.s - 1) * 2.0 * self._nnz() * t
+        return (8 * d + 6) * m * m * n + 4.0 * self._nnz() * m + 6.0 * m * n + chain
 
     def _replay_peak(self, k_done):
         """peak_block_vectors with append-before-trim (solvers.py:163-170) over completed iterations."""

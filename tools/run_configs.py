@@ -1,0 +1,89 @@
+"""Run BASELINE configs 1-5 at full size on one B200 and print one JSON line each.
+
+    python tools/run_configs.py [--configs 1,2,3,4,5] [--kmax-cfg5 20] [--kmax-cfg4 400]
+
+Reports iterations, status, device time, it/s and the SURVEY 8(d) traffic
+model's achieved GB/s against MEASURED_PEAKS.json.  Config 5 runs the lean
+(no A Q cache) scheme: the cached scheme needs ~310 GB.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+import torch
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+import paper_2305_19013_b200 as pk  # noqa: E402
+from paper_2305_19013_b200.engine import DeviceEngine  # noqa: E402
+from paper_2305_19013_b200.problems import make_config  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--configs", default="1,2,3,4,5")
+    ap.add_argument("--kmax-cfg3", type=int, default=None)
+    ap.add_argument("--kmax-cfg4", type=int, default=400)
+    ap.add_argument("--kmax-cfg5", type=int, default=20)
+    ap.add_argument("--repeats", type=int, default=1)
+    args = ap.parse_args()
+    peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
+        else {"hbm_gbs": 6650.0}
+    hbm = float(peaks["hbm_gbs"])
+    fp64 = 37.1e12  # measured DMMA peak (profiles/r01_fp64_peak.txt)
+    for idx in [int(c) for c in args.configs.split(",")]:
+        t0 = time.perf_counter()
+        prob = make_config(idx)
+        build_s = time.perf_counter() - t0
+        kw = dict(prob.solver_kwargs)
+        kmax = {3: args.kmax_cfg3, 4: args.kmax_cfg4, 5: args.kmax_cfg5}.get(idx)
+        if kmax:
+            kw["kmax"] = kmax
+        cfg = pk.SolverConfig(**kw)
+        op = prob.stencil()
+        b = torch.as_tensor(prob.b, device="cuda")
+        best = None
+        for _ in range(args.repeats):
+            eng = DeviceEngine(op, prob.partition, cfg)
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            x, rep = eng.solve(b, x_star=prob.x_star)
+            e1.record()
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            if best is None or ms < best[0]:
+                best = (ms, rep, eng)
+        ms, rep, eng = best
+        secs = ms / 1e3
+        rel_true = rep.true_residual / float(np.linalg.norm(prob.b))
+        t_hbm = rep.model_bytes / (hbm * 1e9)
+        t_fp = rep.model_flops / fp64
+        line = {
+            "config": prob.name, "n": prob.n, "t": kw["t"], "s": kw.get("s", 1), "kmax": kw.get("kmax"),
+            "status": rep.status, "iterations": rep.iterations, "ms": round(ms, 2),
+            "it_per_s": rep.iterations / secs if secs else None,
+            "rel_residual": float(rep.residual_history[-1] / rep.residual_history[0]),
+            "rel_true_residual": rel_true, "relative_error": rep.relative_error,
+            "peak_block_vectors": rep.peak_block_vectors, "lean": bool(eng.lean),
+            "model_GB": rep.model_bytes / 1e9, "model_TF": rep.model_flops / 1e12,
+            "achieved_GBs": rep.model_bytes / secs / 1e9, "hbm_frac": t_hbm / secs,
+            "fp64_frac": t_fp / secs, "roofline_frac": max(t_hbm, t_fp) / secs,
+            "max_mem_GB": torch.cuda.max_memory_allocated() / 1e9, "setup_s": round(build_s, 1),
+            "history_head": [float(v) for v in rep.residual_history[:6]],
+        }
+        print(json.dumps(line), flush=True)
+        del eng, rep, best, x, b, op, prob
+        torch.cuda.empty_cache()
+        torch.cuda.reset_peak_memory_stats()
+
+
+if __name__ == "__main__":
+    main()
