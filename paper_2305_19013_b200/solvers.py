@@ -197,6 +197,9 @@ def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iter
     if partition is None:
         raise ValueError("enlarged methods need a partition")
     cfg.validate(partition)
+    from .partition import Partition
+    if not isinstance(partition, Partition):  # e.g. an ekcg.Partition: adopt its owner map
+        partition = Partition.from_owner(np.asarray(partition.owner()), partition.t)
     n = int(A.n)
     if partition.n != n:
         raise ValueError(f"partition covers {partition.n} indices, matrix has {n}")
