@@ -7,9 +7,9 @@ complete solve to tol (111 iterations); value = iterations / device time.
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--edge E]
   python bench.py --impl reference ...   # the reference algorithm on the host CPU (oracle port)
 
-Under torchrun (N > 1) every rank runs an independent replica of the solve on
-its own GPU (row-sharded multi-GPU is not built yet -- DESIGN.md); timing is
-the max over ranks and value aggregates all ranks.
+Under torchrun (N > 1) the rows are sharded across the ranks (one solve,
+strong scaling: halo exchange + NCCL allreduce, paper_2305_19013_b200/sharded.py);
+timing is the max over ranks.  --form csr falls back to independent replicas.
 """
 
 from __future__ import annotations
@@ -235,8 +235,14 @@ def run_ours(args):
     flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)  # 256 MB > L2 (126 MB)
     timer = KernelTimer(torch, ["hist_gram", "hist_update"])
 
+    from paper_2305_19013_b200.sharded import ShardedEngine
+    sharded = world > 1 and args.form == "stencil"
+
     def solve_once(timed):
-        eng = DeviceEngine(op, prob.partition, cfg, device=dev)
+        if sharded:  # rows split across the ranks (strong scaling of one solve)
+            eng = ShardedEngine(op, prob.partition, cfg, device=dev)
+        else:
+            eng = DeviceEngine(op, prob.partition, cfg, device=dev)
         eng.kernel_timer = timer
         timer.enabled = timed
         x, rep = eng.solve(b_dev)
@@ -255,6 +261,7 @@ def run_ours(args):
     clocks.start()
     launches0 = _lib.query("ekcg_launch_count")
     step_ms, iters, reps, dgram = [], 0, [], []
+    n_rows = prob.n
     for _ in range(args.steps):
         flush.fill_(1.0)  # L2 flush between timed steps (outside the events)
         barrier()
@@ -268,6 +275,7 @@ def run_ours(args):
         iters += rep.iterations
         reps.append(rep)
         dgram.extend(kd for kd in eng.launch_k if kd[0] <= rep.iterations)
+        n_rows = eng.n  # local rows on a shard
     barrier()
     launches = _lib.query("ekcg_launch_count") - launches0
     clk = clocks.stop()
@@ -279,13 +287,14 @@ def run_ours(args):
         tot_ms = float(t.item())
         it_t = torch.tensor([iters], device=dev, dtype=torch.float64)
         dist.all_reduce(it_t)
-        iters_all = int(it_t.item())
+        # sharded: all ranks iterate the same solve; replicas: independent solves
+        iters_all = int(it_t.item()) // world if sharded else int(it_t.item())
     else:
         iters_all = iters
     value = iters_all / (tot_ms / 1e3)
 
     # ---- roofline of the dominant kernel (algorithmic bytes / event-timed duration) ----
-    n, m = prob.n, prob.solver_kwargs["t"] * prob.solver_kwargs.get("s", 1)
+    n, m = n_rows, prob.solver_kwargs["t"] * prob.solver_kwargs.get("s", 1)
     totals = timer.totals_ms()
     counts = timer.counts()
     bytes_alg = {"hist_gram": 0.0, "hist_update": 0.0}
@@ -332,7 +341,8 @@ def run_ours(args):
             t = torch.tensor([e2e_tot], device=dev, dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_tot = float(t.item())
-            e2e_it *= world
+            if not sharded:
+                e2e_it *= world
         e2e = {"value": e2e_it / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
                "d2h_bytes_per_step": 8 * n + 8 * (reps[-1].iterations + 1)}
 
@@ -349,10 +359,12 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": tot_ms / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
             "config": {"workload": prob.name, "form": args.form, "n": n, "t": prob.solver_kwargs["t"],
                        "s": prob.solver_kwargs.get("s", 1), "iterations_per_step": reps[-1].iterations,
-                       "status": reps[-1].status, "parallelism": "replicas" if world > 1 else "single",
+                       "status": reps[-1].status,
+                       "parallelism": (f"rows{world}" if sharded else "replicas") if world > 1 else "single",
                        "l2": "flushed (256 MB write) before every timed step",
                        "time_to_solution_ms": tot_ms / args.steps},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,

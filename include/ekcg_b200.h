@@ -27,7 +27,12 @@ extern "C" {
  * operator (generators.py:25-60) with per-axis coefficients c* (1.0 = the
  * reference) and node conductivity kappa(x,y,z) = kfield[(z/tz*fy + y/ty)*fx
  * + x/tx] (kfield == NULL: kappa = kconst).  dim = 2 (nz ignored) or 3.
- * Grid ordering is x-fastest (generators.py:9). */
+ * Grid ordering is x-fastest (generators.py:9).
+ * Rows [row_begin, row_end) are computed (row_end <= 0: all n rows).  Every
+ * row-indexed pointer passed with a stencil descriptor is addressed by GLOBAL
+ * row: element (i, c) of X is X[i*ldx + c] for the rows the stencil touches,
+ * i.e. [row_begin - nx*ny, row_end + nx*ny) in 3-D -- a row shard passes a
+ * base pointer shifted by its first row (halo planes included). */
 typedef struct EkcgStencil {
     int dim;
     int nx, ny, nz;
@@ -36,6 +41,7 @@ typedef struct EkcgStencil {
     int tx, ty, tz;
     int fx, fy;
     double kconst;
+    long long row_begin, row_end;
 } EkcgStencil;
 
 /* ---- sparse operator and T^t split ------------------------------------ */
@@ -142,9 +148,12 @@ int ekcg_update_vec(const double* const* Qs, int ldq, const double* S, double* W
                     void* stream);
 
 /* G = X^T (A X) for the stencil operator without materialising A X, fused
- * with the A-CholQR factor S = chol(sym G)^-1 (aortho.py:107-109). ldx == m. */
+ * with the A-CholQR factor S = chol(sym G)^-1 (aortho.py:107-109). ldx == m.
+ * finalize = 0 writes the (local) G to `out` instead -- a row shard
+ * allreduces it and calls ekcg_cholinv. */
 int ekcg_stencil_cholinv(const EkcgStencil* desc, const double* X, int ldx, int m, double* partials,
-                         unsigned int* counter, double* S, void* ctrl, int iteration, double tol, void* stream);
+                         unsigned int* counter, double* out, void* ctrl, int iteration, double tol, int finalize,
+                         void* stream);
 
 /* Y = A X (written) fused with x += X alpha, r -= Y alpha, |r|^2 and, when
  * do_finish, the end-of-iteration bookkeeping of ekcg_finish (else |r|^2 is

@@ -48,7 +48,7 @@ SIGNATURES = {
     "ekcg_update_vec": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_longlong, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_void_p]),
     "ekcg_stencil_cholinv": (c_int, [c_void_p, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_void_p,
-                                     c_int, c_double, c_void_p]),
+                                     c_int, c_double, c_int, c_void_p]),
     "ekcg_stencil_xr": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_void_p,
                                 c_void_p]),
@@ -65,6 +65,7 @@ class EkcgStencil(ctypes.Structure):
         ("tx", c_int), ("ty", c_int), ("tz", c_int),
         ("fx", c_int), ("fy", c_int),
         ("kconst", c_double),
+        ("row_begin", c_longlong), ("row_end", c_longlong),
     ]
 
 

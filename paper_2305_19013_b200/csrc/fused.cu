@@ -225,7 +225,7 @@ template <int VEC, int M>
 __global__ void __launch_bounds__(256)
 stencil_cholinv_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X, int ldx,
                        double* __restrict__ partials, unsigned int* counter, double* Sout, EkcgCtrl* ctrl,
-                       int iteration, double tol) {
+                       int iteration, double tol, int finalize) {
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
     constexpr int G = M / VEC;
@@ -253,10 +253,10 @@ stencil_cholinv_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict_
 #pragma unroll
         for (int b = 0; b < GBT; ++b) gacc[a][b][0] = gacc[a][b][1] = 0.0;
 
-    const long long n = (long long)s.nx * s.ny * s.nz;
+    const long long n = s.row_end;
     const int c0 = threadIdx.x * VEC;
     const int ty = threadIdx.y;
-    for (long long base = (long long)blockIdx.x * R; base < n; base += (long long)gridDim.x * R) {
+    for (long long base = s.row_begin + (long long)blockIdx.x * R; base < n; base += (long long)gridDim.x * R) {
         const long long i = base + ty;
         double y[VEC];
         if (i < n) {
@@ -299,9 +299,13 @@ stencil_cholinv_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict_
         partials[(long long)blockIdx.x * M * M + o] = sacc;
     }
     if (last_cta_arrive(counter)) {
-        double* Gm = sm;
-        cta_sum_partials_mlp(partials, gridDim.x * gridDim.y, M * M, Gm);
-        cholinv_body(Gm, Gm + M * M, Gm + 2 * M * M, M, Sout, ctrl, iteration, tol);
+        if (!finalize) {
+            cta_sum_partials_mlp(partials, gridDim.x * gridDim.y, M * M, Sout);  // local G
+        } else {
+            double* Gm = sm;
+            cta_sum_partials_mlp(partials, gridDim.x * gridDim.y, M * M, Gm);
+            cholinv_body(Gm, Gm + M * M, Gm + 2 * M * M, M, Sout, ctrl, iteration, tol);
+        }
     }
 }
 
@@ -320,10 +324,11 @@ stencil_xr_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X, 
     for (int a = tid; a < m; a += 256) sa[a] = alpha[a];
     __syncthreads();
     const int G = blockDim.x;
-    const long long n = (long long)s.nx * s.ny * s.nz;
+    const long long n = s.row_end;
     const int c0 = threadIdx.x * VEC;
     double sq = 0.0;
-    for (long long base = (long long)blockIdx.x * blockDim.y; base < n; base += (long long)gridDim.x * blockDim.y) {
+    for (long long base = s.row_begin + (long long)blockIdx.x * blockDim.y; base < n;
+         base += (long long)gridDim.x * blockDim.y) {
         const long long i = base + threadIdx.y;
         double dx = 0.0, dr = 0.0;
         if (i < n) {
@@ -416,7 +421,7 @@ int launch_update_epi(const double* const* Qs, int ldq, int d, const double* C, 
 template <int VEC, int M>
 int launch_stencil_cholinv(const EkcgStencil& s, const UniformFaces& uf, long long n, const double* X, int ldx,
                            double* partials, unsigned int* counter, double* Sout, EkcgCtrl* ctrl, int iteration,
-                           double tol, cudaStream_t st) {
+                           double tol, int finalize, cudaStream_t st) {
     constexpr int G = M / VEC;
     constexpr int R = 256 / G;
     constexpr int LDS = pad_stride(M);
@@ -430,7 +435,7 @@ int launch_stencil_cholinv(const EkcgStencil& s, const UniformFaces& uf, long lo
     if (!set_smem((const void*)fn, smem)) return EKCG_ELAUNCH;
     long long blocks = (n + R - 1) / R;
     int grid = (int)(blocks < kFusedCtas ? blocks : kFusedCtas);
-    fn<<<grid, dim3(G, R), smem, st>>>(s, uf, X, ldx, partials, counter, Sout, ctrl, iteration, tol);
+    fn<<<grid, dim3(G, R), smem, st>>>(s, uf, X, ldx, partials, counter, Sout, ctrl, iteration, tol, finalize);
     return EKCG_OK;
 }
 
@@ -485,7 +490,7 @@ extern "C" int ekcg_update_vec(const double* const* Qs, int ldq, const double* S
 
 extern "C" int ekcg_stencil_cholinv(const EkcgStencil* desc, const double* X, int ldx, int m, double* partials,
                                     unsigned int* counter, double* S, void* ctrl, int iteration, double tol,
-                                    void* stream) {
+                                    int finalize, void* stream) {
     EkcgStencil s;
     UniformFaces uf;
     long long n;
@@ -494,11 +499,12 @@ extern "C" int ekcg_stencil_cholinv(const EkcgStencil* desc, const double* X, in
     if (ldx != m || ((reinterpret_cast<uintptr_t>(X) & 15) != 0) || ctrl == nullptr) return EKCG_EINVAL;
     EkcgCtrl* c = (EkcgCtrl*)ctrl;
     cudaStream_t st = as_stream(stream);
+    n = s.row_end - s.row_begin;
     switch (m) {
-        case 8: rc = launch_stencil_cholinv<4, 8>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, st); break;
-        case 16: rc = launch_stencil_cholinv<4, 16>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, st); break;
-        case 32: rc = launch_stencil_cholinv<4, 32>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, st); break;
-        case 64: rc = launch_stencil_cholinv<4, 64>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, st); break;
+        case 8: rc = launch_stencil_cholinv<4, 8>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, finalize, st); break;
+        case 16: rc = launch_stencil_cholinv<4, 16>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, finalize, st); break;
+        case 32: rc = launch_stencil_cholinv<4, 32>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, finalize, st); break;
+        case 64: rc = launch_stencil_cholinv<4, 64>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, finalize, st); break;
         default: return EKCG_EINVAL;
     }
     if (rc != EKCG_OK) return rc;
@@ -528,6 +534,7 @@ extern "C" int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx
     while (gp < g) gp <<= 1;  // threads per row: power of two so a row's lanes are shuffle-aligned
     if (gp > 32) return EKCG_EINVAL;
     dim3 block(gp, 256 / gp);
+    n = s.row_end - s.row_begin;
     long long blocks = (n + block.y - 1) / block.y;
     int grid = (int)(blocks < kFusedCtas ? blocks : kFusedCtas);
     if (vec == 4)

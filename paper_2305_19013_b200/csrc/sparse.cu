@@ -151,9 +151,9 @@ __global__ void __launch_bounds__(256)
 stencil_spmm_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X, int ldx,
                     double* __restrict__ Y, int ldy, int m, const int* __restrict__ live) {
     EKCG_GATE(live);
-    const long long n = (long long)s.nx * s.ny * s.nz;
     const int c0 = threadIdx.x * VEC;
-    ROW_LOOP(i, n) {
+    for (long long i = s.row_begin + (long long)blockIdx.x * blockDim.y + threadIdx.y; i < s.row_end;
+         i += (long long)gridDim.x * blockDim.y) {
         long long off[7];
         double val[7];
         int dpos;
@@ -218,6 +218,7 @@ extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int l
     cudaStream_t st = as_stream(stream);
     const bool aligned = (ldx % 2 == 0) && (ldy % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+    n = s.row_end - s.row_begin;
     if (aligned && m % 4 == 0) {
         RowLaunch L = row_launch(n, m / 4);
         stencil_spmm_kernel<4><<<L.grid, L.block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, live);

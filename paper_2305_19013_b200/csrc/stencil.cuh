@@ -154,6 +154,11 @@ static inline int prepare_stencil(const EkcgStencil* desc, EkcgStencil& s, Unifo
     if (s.kfield != nullptr && (s.tx < 1 || s.ty < 1 || s.tz < 1 || s.fx < 1 || s.fy < 1)) return EKCG_EINVAL;
     n = (long long)s.nx * s.ny * s.nz;
     if (n >= (1LL << 32)) return EKCG_EINVAL;
+    if (s.row_end <= 0) {
+        s.row_begin = 0;
+        s.row_end = n;
+    }
+    if (s.row_begin < 0 || s.row_begin >= s.row_end || s.row_end > n) return EKCG_EINVAL;
     uf = UniformFaces{};
     if (s.kfield == nullptr) {
         uf.fz = host_face(s.cz, s.kconst);

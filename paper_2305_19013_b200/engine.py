@@ -343,7 +343,7 @@ class DeviceEngine:
             # G = W0^T A W0 (A W0 never written) + A-CholQR factor S
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WB, m, m, part.data_ptr(), self.counter.data_ptr(),
-                self.S.data_ptr(), live, k, 1e-14, st))
+                self.S.data_ptr(), live, k, 1e-14, 1, st))
         else:
             self._apply_op(WB, m, WC, m, m)
             self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_self")
@@ -427,7 +427,7 @@ class DeviceEngine:
         if fused:
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WC, m, m, part.data_ptr(), self.counter.data_ptr(),
-                self.S.data_ptr(), live, k, 1e-14, st))
+                self.S.data_ptr(), live, k, 1e-14, 1, st))
             self._timed("tri_alpha", lambda: _lib.call(
                 "ekcg_update_vec", WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
                 part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
@@ -540,19 +540,7 @@ class DeviceEngine:
         ev0 = torch.cuda.Event(enable_timing=True)
         ev1 = torch.cuda.Event(enable_timing=True)
         ev0.record()
-        self.b = torch.as_tensor(b, dtype=torch.float64).to(dev, non_blocking=False).contiguous()
-        if x0 is None:
-            self.x = torch.zeros(self.n, dtype=torch.float64, device=dev)
-        else:
-            self.x = torch.as_tensor(x0, dtype=torch.float64).to(dev).clone().contiguous()
-        self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
-        st = self.stream
-        # r = b - A x ; rho0 = |r|  (solvers.py:341-343)
-        self._apply_op(self.x.data_ptr(), 1, self.tmpv.data_ptr(), 1, 1, tag="spmv", live=None)
-        _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), self.r.data_ptr(), self.n, None, st)
-        _lib.call("ekcg_sumsq", self.r.data_ptr(), self.n, self.vpart.data_ptr(), None, st)
-        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), None, st)
-        _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
+        self._begin(b, x0)
 
         sync_each = (on_iteration is not None or self.retention == "restart-tol"
                      or cfg.switch_tol is not None or self.sync_mode)
@@ -599,6 +587,38 @@ class DeviceEngine:
         solve_s = ev0.elapsed_time(ev1) / 1e3
         return self._report(ctrl, x_star, numpy_io, solve_s, time.perf_counter() - t_wall0)
 
+    def _begin(self, b, x0):
+        """Upload b / x0, r = b - A x, rho0 = |r| and the control block (solvers.py:341-345)."""
+        dev, st = self.device, self.stream
+        self.b = torch.as_tensor(b, dtype=torch.float64).to(dev, non_blocking=False).contiguous()
+        if x0 is None:
+            self.x = torch.zeros(self.n, dtype=torch.float64, device=dev)
+        else:
+            self.x = torch.as_tensor(x0, dtype=torch.float64).to(dev).clone().contiguous()
+        self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
+        self._apply_op(self.x.data_ptr(), 1, self.tmpv.data_ptr(), 1, 1, tag="spmv", live=None)
+        _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), self.r.data_ptr(), self.n, None, st)
+        _lib.call("ekcg_sumsq", self.r.data_ptr(), self.n, self.vpart.data_ptr(), None, st)
+        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), None, st)
+        self._allreduce(self.rho2)
+        _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
+
+    def _allreduce(self, t):
+        """Sum a small partial across row shards (no-op on one GPU)."""
+
+    def _final_metrics(self, x_star):
+        """(|b - A x|, |x - x*| / |x*|) of the final iterate (solvers.py:289-291)."""
+        self._residual_sq(self.x, self.tr2, None)
+        true_res = float(torch.sqrt(self.tr2).item())
+        rel = None
+        if x_star is not None:
+            xs = torch.as_tensor(x_star, dtype=torch.float64).to(self.device)
+            rel = float((torch.linalg.vector_norm(self.x - xs) / torch.linalg.vector_norm(xs)).item())
+        return true_res, rel
+
+    def _output_x(self, numpy_io):
+        return self.x.cpu().numpy() if numpy_io else self.x
+
     def _state(self, k, rho, tol1, numpy_io):
         conv = (lambda t: t.cpu().numpy()) if numpy_io else (lambda t: t.clone())
         blocks = []
@@ -639,14 +659,8 @@ class DeviceEngine:
         nchecks = k_done // self.every
         checks_v = self.checks[:nchecks].cpu().numpy() if nchecks else np.zeros(0)
         checks = [((i + 1) * self.every, float(checks_v[i])) for i in range(nchecks)]
-        # true residual and relative error (solvers.py:289-291)
-        self._residual_sq(self.x, self.tr2, None)
-        true_res = float(torch.sqrt(self.tr2).item())
-        rel = None
-        if x_star is not None:
-            xs = torch.as_tensor(x_star, dtype=torch.float64).to(self.device)
-            rel = float((torch.linalg.vector_norm(self.x - xs) / torch.linalg.vector_norm(xs)).item())
-        x_out = self.x.cpu().numpy() if numpy_io else self.x
+        true_res, rel = self._final_metrics(x_star)
+        x_out = self._output_x(numpy_io)
         model_bytes = sum(self._iter_bytes(d, m) for kk, d, m in self.launch_k if kk <= k_done)
         model_flops = sum(self._iter_flops(d, m) for kk, d, m in self.launch_k if kk <= k_done)
         rep = ConvergenceReport(

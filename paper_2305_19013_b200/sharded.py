@@ -1,0 +1,242 @@
+"""Row-sharded multi-GPU engine: one process per GPU.
+
+Each rank owns a slab of whole grid layers (dist.RowShard) and runs the same
+kernel sequence as engine.DeviceEngine on its local rows:
+
+* blocks that feed the stencil (the candidate / s-step chain block, W0, every
+  retained W_k, x) are stored with one halo layer on each side and exchanged
+  with the neighbours right before each operator application;
+* every split-K reduction (CGS2 coefficients, Graw, G, alpha, |r|^2) is
+  reduced locally, then summed across ranks with one NCCL allreduce, and the
+  m x m factorizations / stop test run redundantly on every rank from
+  identical bytes -- so all ranks take the same decisions;
+* the stencil kernels address rows globally (EkcgStencil.row_begin/row_end),
+  so the same sm_100a kernels serve one GPU and a shard.
+
+Scope: stencil operators, SRE-CG2 / SRE-CG with s >= 1, full / trunc /
+restart retention (the cached-A Q scheme).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .dist import Comm, RowShard
+from .engine import F64, DeviceEngine, _Block
+from .operators import StencilOperator
+
+
+class ShardedEngine(DeviceEngine):
+    def __init__(self, op, partition, cfg, comm=None, device=None):
+        if not isinstance(op, StencilOperator):
+            raise TypeError("the sharded engine needs a StencilOperator")
+        if cfg.method not in ("sre-cg2", "sre-cg") or cfg.switch_tol is not None:
+            raise ValueError("the sharded engine runs SRE-CG2 / SRE-CG without the flexible switch")
+        super().__init__(op, partition, cfg, device=device)
+        self.comm = comm if comm is not None else Comm()
+        self.shard = RowShard(op.shape, self.comm.rank, self.comm.world)
+        self.n_global = op.n
+        self.kmax = cfg.kmax if cfg.kmax is not None else 2 * self.n_global
+        self.stag_window = max(20, self.kmax // 10) if self.retention == "restart" else 0
+        self.n = self.shard.n_local  # every row-local kernel works on the local rows
+        self.cache_aq = True
+        desc = _lib.EkcgStencil()
+        ctypes.memmove(ctypes.byref(desc), ctypes.byref(op._desc), ctypes.sizeof(desc))
+        desc.row_begin, desc.row_end = self.shard.row_begin, self.shard.row_end
+        self._desc = desc
+
+    # ------------------------------------------------------------ pointers
+    def _lptr(self, ext, ld):
+        """Local-row view of an extended (haloed) buffer."""
+        return ext.data_ptr() + F64 * self.shard.halo * ld
+
+    def _gptr_ext(self, ext, ld):
+        """Global-row-addressed pointer into an extended buffer."""
+        return ext.data_ptr() + F64 * (self.shard.halo - self.shard.row_begin) * ld
+
+    def _gptr_loc(self, loc, ld):
+        """Global-row-addressed pointer into a local (halo-free) buffer."""
+        return loc.data_ptr() - F64 * self.shard.row_begin * ld
+
+    def _stencil(self, x_gptr, ldx, y_gptr, ldy, m, live):
+        _lib.call("ekcg_spmm_stencil", ctypes.byref(self._desc), x_gptr, ldx, y_gptr, ldy, m, live, self.stream)
+
+    # --------------------------------------------------------------- setup
+    def _setup(self):
+        super()._setup()
+        ext = self.shard.ext_rows
+        mm = self.m_max
+        f64 = dict(dtype=torch.float64, device=self.device)
+        self.WA = torch.zeros(ext * mm, **f64)   # candidate / s-step chain (stencil input)
+        self.WB = torch.zeros(ext * mm, **f64)   # W0 (stencil input)
+        self.fused_ok = True
+        owner = self.partition.owner()[self.shard.row_begin:self.shard.row_end]
+        self.owner_dev = torch.from_numpy(np.ascontiguousarray(owner, dtype=np.int32)).to(self.device)
+
+    def _new_block(self, width):
+        ext = self.shard.ext_rows
+        f64 = dict(dtype=torch.float64, device=self.device)
+        if self.window is not None:
+            slot = self.since_clear % self.window
+            if slot not in self.slots:
+                self.slots[slot] = (torch.zeros(ext * self.m_max, **f64), torch.empty(self.n * self.m_max, **f64))
+            q, aq = self.slots[slot]
+        else:
+            slot = -1
+            q, aq = torch.zeros(ext * width, **f64), torch.empty(self.n * width, **f64)
+        return _Block(q, aq, width, slot)
+
+    def _allreduce(self, t):
+        self.comm.allreduce_(t)
+
+    # --------------------------------------------------------- residuals
+    def _begin(self, b, x0):
+        dev, st, sh = self.device, self.stream, self.shard
+        b = torch.as_tensor(b, dtype=torch.float64)
+        if b.numel() == self.n_global:
+            b = b[sh.row_begin:sh.row_end]
+        self.b = b.to(dev).contiguous()
+        self.x = torch.zeros(sh.ext_rows, dtype=torch.float64, device=dev)
+        if x0 is not None:
+            x0 = torch.as_tensor(x0, dtype=torch.float64)
+            if x0.numel() == self.n_global:
+                x0 = x0[sh.row_begin:sh.row_end]
+            self.x[sh.halo:sh.halo + sh.n_local].copy_(x0.to(dev))
+        self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
+        self._residual_sq(self.x, self.rho2, None, store_r=True)
+        _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
+
+    def _residual_sq(self, x, out, live, store_r=False):
+        """out = |b - A x|^2 over all ranks (x extended with halos)."""
+        st = self.stream
+        self.comm.halo_exchange(x, 1, self.shard)
+        self._stencil(self._gptr_ext(x, 1), 1, self._gptr_loc(self.tmpv, 1), 1, 1, live)
+        dst = self.r if store_r else self.tmpv
+        _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), dst.data_ptr(), self.n, live, st)
+        _lib.call("ekcg_sumsq", dst.data_ptr(), self.n, self.vpart.data_ptr(), live, st)
+        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, out.data_ptr(), live, st)
+        self.comm.allreduce_(out)
+
+    def _final_metrics(self, x_star):
+        self._residual_sq(self.x, self.tr2, None)
+        true_res = float(torch.sqrt(self.tr2).item())
+        rel = None
+        if x_star is not None:
+            sh = self.shard
+            xs = torch.as_tensor(x_star, dtype=torch.float64)[sh.row_begin:sh.row_end].to(self.device)
+            xl = self.x[sh.halo:sh.halo + sh.n_local]
+            sums = torch.stack([torch.sum((xl - xs) ** 2), torch.sum(xs ** 2)])
+            self.comm.allreduce_(sums)
+            rel = float(torch.sqrt(sums[0] / sums[1]).item())
+        return true_res, rel
+
+    def _output_x(self, numpy_io):
+        sh = self.shard
+        full = self.comm.gather_rows(self.x[sh.halo:sh.halo + sh.n_local].contiguous(), sh)
+        return full.cpu().numpy() if numpy_io else full
+
+    def _state(self, k, rho, tol1, numpy_io):
+        raise NotImplementedError("on_iteration callbacks are not available on the sharded engine")
+
+    # ----------------------------------------------------------- iteration
+    def _enqueue_iteration(self, k, tol1):
+        cfg, n, st, live = self.cfg, self.n, self.stream, self.live
+        if k > 1 and self.retention == "restart" and k % cfg.restart_j == 1:
+            self._clear()
+            self.restarts.append(k)
+        elif (k > 1 and self.retention == "restart-tol" and tol1 < cfg.restart_tol
+              and (not self.restarts or k > self.restarts[-1] + 1)):
+            self._clear()
+            self.restarts.append(k)
+        t = self.t_cur
+        m = self.s * t
+        d = len(self.retained)
+        newest = self.retained[-1] if self.retained else None
+        blk = self._new_block(m)
+        lWA, lWB = self._lptr(self.WA, m), self._lptr(self.WB, m)
+        lq = lambda b: self._lptr(b.q, b.width)
+        ptrs = [lq(b) for b in self.retained] + [b.aq.data_ptr() for b in self.retained] + [lWA, lWB, lq(blk)]
+        base = self.arena.push(ptrs)
+        q_addr = lambda i: base + F64 * i
+        aq_addr = lambda i: base + F64 * (d + i)
+        WA_arr, WB_arr, NEW_arr = (base + F64 * (2 * d + j) for j in range(3))
+
+        # ---- candidate ----
+        fresh = not self.retained
+        W = lWA
+        if fresh:
+            _lib.call("ekcg_split", self.r.data_ptr(), self.owner_dev.data_ptr(), lWA, n, t, m, live, st)
+            self._chain_sharded(m, t, live)
+        elif self.s == 1:
+            W = newest.aq.data_ptr()
+        else:
+            _lib.call("ekcg_copy_cols", newest.aq.data_ptr() + F64 * (newest.width - t), newest.width, lWA, m,
+                      n, t, live, st)
+            self._chain_sharded(m, t, live)
+
+        # ---- CGS2 (aortho.py:89-95): local Grams, one allreduce per pass ----
+        if d > 0:
+            C = self._ensure("C", d * m * m)
+            for _ in range(2):
+                self._gram(aq_addr(0), m, d, m, W, m, m, C.data_ptr(), tag="hist_gram")
+                self.comm.allreduce_(C[: d * m * m])
+                self._update(q_addr(0), m, d, m, C.data_ptr(), W, m, lWA, m, m, 1.0, -1.0, tag="hist_update")
+                W = lWA
+
+        # ---- Pre-CholQR ----
+        self._gram(WA_arr, m, 1, m, lWA, m, m, self.Graw.data_ptr(), tag="gram_self")
+        self.comm.allreduce_(self.Graw[: m * m])
+        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+        self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, lWB, m, m, 0.0, 1.0, tag="tri_apply")
+        self.comm.halo_exchange(self.WB, m, self.shard)
+        fused = m in (8, 16, 32, 64)
+        part = self._ensure("part", max(self.fused_part, 1)) if fused else None
+        if fused:
+            _lib.call("ekcg_stencil_cholinv", ctypes.byref(self._desc), self._gptr_ext(self.WB, m), m, m,
+                      part.data_ptr(), self.counter.data_ptr(), self.G.data_ptr(), live, k, 1e-14, 0, st)
+        else:
+            self._stencil(self._gptr_ext(self.WB, m), m, self._gptr_loc(self.WC, m), m, m, live)
+            self._gram(WB_arr, m, 1, m, self.WC.data_ptr(), m, m, self.G.data_ptr(), tag="gram_self")
+        self.comm.allreduce_(self.G[: m * m])
+        _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+        if fused:
+            _lib.call("ekcg_update_vec", WB_arr, m, self.S.data_ptr(), lq(blk), m, m, n, self.r.data_ptr(),
+                      part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st)
+        else:
+            self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, lq(blk), m, m, 0.0, 1.0, tag="tri_apply")
+            self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
+        self.comm.allreduce_(self.alpha[:m])
+
+        # ---- AW_k = A W_k and the iterate update ----
+        self.comm.halo_exchange(blk.q, m, self.shard)
+        if fused:
+            _lib.call("ekcg_stencil_xr", ctypes.byref(self._desc), self._gptr_ext(blk.q, m), m,
+                      self._gptr_loc(blk.aq, m), m, m, self.alpha.data_ptr(), self._gptr_ext(self.x, 1),
+                      self._gptr_loc(self.r, 1), part.data_ptr(), self.counter.data_ptr(), live, k, self.kmax,
+                      self.stag_window, self.history.data_ptr(), 0, self.rho2.data_ptr(), st)
+        else:
+            self._stencil(self._gptr_ext(blk.q, m), m, self._gptr_loc(blk.aq, m), m, m, live)
+            _lib.call("ekcg_xr_update", lq(blk), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
+                      self._lptr(self.x, 1), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st)
+            _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
+        self.comm.allreduce_(self.rho2)
+        self._append(blk)
+        if k % self.every == 0:
+            slot = k // self.every - 1
+            self._ensure_checks(slot + 1)
+            self._residual_sq(self.x, self.tr2, live)
+            _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
+        self._ensure_history(k + 1)
+        _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+                  self.history.data_ptr(), st)
+        self._account(k, d, m, fresh, t)
+
+    def _chain_sharded(self, m, t, live):
+        g = lambda col: self._gptr_ext(self.WA, m) + F64 * col
+        for i in range(1, self.s):
+            self.comm.halo_exchange(self.WA, m, self.shard)
+            self._stencil(g((i - 1) * t), m, g(i * t), m, t, live)

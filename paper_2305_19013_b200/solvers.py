@@ -207,5 +207,13 @@ def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iter
     x0 = _as_float_vec(x0, n, "x0")
     if cfg.preconditioner is not None:
         raise NotImplementedError("split block-Jacobi preconditioning is not on the device path yet")
-    engine = DeviceEngine(A, partition, cfg, device=device)
+    import torch.distributed as tdist
+    from .operators import StencilOperator
+    sharded = (tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1
+               and isinstance(A, StencilOperator))
+    if sharded:  # one process per GPU, rows split across ranks
+        from .sharded import ShardedEngine
+        engine = ShardedEngine(A, partition, cfg, device=device)
+    else:
+        engine = DeviceEngine(A, partition, cfg, device=device)
     return engine.solve(b, x0, x_star=x_star, on_iteration=on_iteration)

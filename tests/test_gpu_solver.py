@@ -285,3 +285,24 @@ def test_lean_scheme_matches_cached(floors_golden, solves_golden, idx, edge, for
     assert hist_dev(rep.residual_history, arrays[f"{name}__history"]) <= hist_tol(floors_golden, name)
     assert abs(rep.iterations - ref["iterations"]) <= iter_tol(floors_golden, name, ref["iterations"])
     assert rep.peak_block_vectors == ref["peak_block_vectors"] or rep.iterations != ref["iterations"]
+
+
+@pytest.mark.parametrize("idx,edge,over", [(2, 16, {}), (3, 16, {}), (4, 10, {}), (1, 40, {}),
+                                           (2, 12, {"retention": "restart", "restart_j": 5})])
+def test_sharded_engine_single_rank_matches(idx, edge, over):
+    """The row-sharded engine (halo'd blocks, global-row stencil addressing,
+    allreduce points) on one rank follows the single-GPU engine."""
+    from paper_2305_19013_b200.engine import DeviceEngine
+    from paper_2305_19013_b200.sharded import ShardedEngine
+    prob = make_config(idx, edge)
+    cfg = SolverConfig(**dict(prob.solver_kwargs, **over))
+    op = prob.stencil()
+    _, ref = DeviceEngine(op, prob.partition, cfg).solve(prob.b, x_star=prob.x_star)
+    x, rep = ShardedEngine(op, prob.partition, cfg).solve(prob.b, x_star=prob.x_star)
+    assert rep.status == ref.status
+    assert rep.iterations == ref.iterations
+    assert hist_dev(rep.residual_history, ref.residual_history) <= 1e-10
+    assert rep.peak_block_vectors == ref.peak_block_vectors
+    assert rep.restart_iterations == ref.restart_iterations
+    assert abs(rep.true_residual - ref.true_residual) <= 1e-6 * ref.true_residual + 1e-300
+    assert x.shape == (prob.n,)
