@@ -173,44 +173,43 @@ def run_reference(args):
 # GPU leg
 # ---------------------------------------------------------------------------
 class KernelTimer:
-    """CUDA-event timing of selected kernel launches on the launching stream.
+    """CUDA-event timing of the CGS2 history kernels on the launching stream.
 
-    Events come from a pool created up front (no allocation in the timed
-    region); elapsed times are harvested after each step's final sync.
+    Only launches of the GPU-bound phase (d >= d_min retained blocks) are
+    bracketed, so the host cost of the event records hides behind device work;
+    events come from a pool created up front and are harvested after each
+    step's final sync.  Each record keeps (tag, k, d, m) for the byte count.
     """
 
-    def __init__(self, torch, tags, pool=4096):
+    def __init__(self, torch, tags, d_min=16, pool=4096):
         self.torch = torch
         self.tags = set(tags)
+        self.d_min = d_min
         self.pool = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
                      for _ in range(pool)]
         self.used = []
-        self.ms = {tag: 0.0 for tag in tags}
-        self.n = {tag: 0 for tag in tags}
+        self.records = []  # (tag, k, d, m, ms)
         self.enabled = False
+        self.engine = None
 
     def __call__(self, tag, fn):
-        if not self.enabled or tag not in self.tags or len(self.used) >= len(self.pool):
+        cur = getattr(self.engine, "_cur", None)
+        if (not self.enabled or tag not in self.tags or cur is None or cur[1] < self.d_min
+                or len(self.used) >= len(self.pool)):
             fn()
             return
         e0, e1 = self.pool[len(self.used)]
         e0.record()
         fn()
         e1.record()
-        self.used.append(tag)
+        self.used.append((tag,) + tuple(cur))
 
-    def harvest(self):
-        """Call after a full device sync."""
-        for tag, (e0, e1) in zip(self.used, self.pool):
-            self.ms[tag] += e0.elapsed_time(e1)
-            self.n[tag] += 1
+    def harvest(self, k_done):
+        """Call after a full device sync; drops launches past the stopping iteration."""
+        for (tag, k, d, m), (e0, e1) in zip(self.used, self.pool):
+            if k <= k_done:
+                self.records.append((tag, k, d, m, e0.elapsed_time(e1)))
         self.used = []
-
-    def totals_ms(self):
-        return dict(self.ms)
-
-    def counts(self):
-        return dict(self.n)
 
 
 def run_ours(args):
@@ -244,6 +243,7 @@ def run_ours(args):
         else:
             eng = DeviceEngine(op, prob.partition, cfg, device=dev)
         eng.kernel_timer = timer
+        timer.engine = eng
         timer.enabled = timed
         x, rep = eng.solve(b_dev)
         return rep, eng
@@ -270,7 +270,7 @@ def run_ours(args):
         rep, eng = solve_once(True)
         e1.record()
         e1.synchronize()
-        timer.harvest()
+        timer.harvest(rep.iterations)
         step_ms.append(e0.elapsed_time(e1))
         iters += rep.iterations
         reps.append(rep)
@@ -294,20 +294,24 @@ def run_ours(args):
     value = iters_all / (tot_ms / 1e3)
 
     # ---- roofline of the dominant kernel (algorithmic bytes / event-timed duration) ----
-    n, m = n_rows, prob.solver_kwargs["t"] * prob.solver_kwargs.get("s", 1)
-    totals = timer.totals_ms()
-    counts = timer.counts()
-    bytes_alg = {"hist_gram": 0.0, "hist_update": 0.0}
-    for k, d, mm in dgram:
-        if d > 0:
-            bytes_alg["hist_gram"] += 2 * 8.0 * (d + 1) * n * mm      # two passes: read AQ_1..d and W
-            bytes_alg["hist_update"] += 2 * 8.0 * (d + 2) * n * mm    # two passes: read Q_1..d, W; write W
-    dom = max(("hist_gram", "hist_update"), key=lambda k: totals.get(k, 0.0))
+    m = prob.solver_kwargs["t"] * prob.solver_kwargs.get("s", 1)
+    n = n_rows
+    per_tag = {}
+    for tag, k, d, mm, ms in timer.records:
+        # Gram reads A Q_1..d and W; the update reads Q_1..d, W and writes W'
+        bytes_ = 8.0 * (d + 1) * n * mm if tag == "hist_gram" else 8.0 * (d + 2) * n * mm
+        flops = 2.0 * d * mm * mm * n
+        acc = per_tag.setdefault(tag, [0.0, 0.0, 0.0, 0])
+        acc[0] += bytes_
+        acc[1] += flops
+        acc[2] += ms
+        acc[3] += 1
+    dom = max(per_tag, key=lambda t: per_tag[t][2]) if per_tag else None
     hbm, peak_kind = peaks()
-    achieved = bytes_alg[dom] / (totals[dom] / 1e3) / 1e9 if totals.get(dom) else None
+    achieved = per_tag[dom][0] / (per_tag[dom][2] / 1e3) / 1e9 if dom else None
     prof = ROOT / "profiles" / "r01_traffic.json"
     traffic = None
-    if prof.exists():
+    if prof.exists() and dom:
         traffic = json.loads(prof.read_text()).get(dom)
     model_bytes = sum(r.model_bytes for r in reps)
     model_time = model_bytes / (hbm * 1e9)
@@ -315,8 +319,9 @@ def run_ours(args):
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "kernel": dom,
         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
-        "kernel_ms_total": {k: round(v, 3) for k, v in totals.items()},
-        "kernel_launches": counts,
+        "per_kernel": {t: {"GBs": v[0] / (v[2] / 1e3) / 1e9, "TFLOPs": v[1] / (v[2] / 1e3) / 1e12,
+                           "ms_total": round(v[2], 3), "launches": v[3]} for t, v in per_tag.items()},
+        "timed_launches": f"CGS2 launches with d >= {timer.d_min} retained blocks, all timed steps",
         "step_model_gbs": model_bytes / (tot_ms / 1e3) / 1e9,
         "step_model_frac": model_time / (tot_ms / 1e3),
     }

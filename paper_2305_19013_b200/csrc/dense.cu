@@ -46,18 +46,6 @@ int gram_blocks_per_cta(int d, int m1, int m2) {
     return gb;
 }
 
-int gram_chunks(long long n, int d, int m1, int m2) {
-    const int gb = gram_blocks_per_cta(d, m1, m2);
-    const long long groups = (d + gb - 1) / gb;
-    long long target = g_gram_target;
-    if (target <= 0) target = (m1 == 16 && m2 == 16 && d >= 48) ? 148LL * 8 : 148LL * 4;
-    long long p = (target + groups - 1) / groups;
-    long long max_p = (n + 255) / 256;
-    if (p > max_p) p = max_p;
-    if (p < 1) p = 1;
-    return (int)p;
-}
-
 // ---------------------------------------------------------------------------
 // DMMA Gram: partials[p][i] (M x M) = X_i[rows of p]^T Y[rows of p]
 // CTA (p, g) handles row chunk p for blocks i = g*GB .. g*GB+GB-1, so each Y
@@ -165,6 +153,77 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
             partials[((long long)blockIdx.x * d + i0 + g) * (M * M) + e] = s;
         }
     }
+}
+
+using GramFn = void (*)(const double* const*, int, int, const double*, int, long long, long long, double*,
+                        const int*);
+
+// The DMMA Gram variant for (d, m1, m2) (nullptr: generic kernel) and its GB.
+GramFn select_gram(int d, int m1, int m2, int& gb) {
+    gb = gram_blocks_per_cta(d, m1, m2);
+    if (m1 != m2) return nullptr;
+    switch (m1) {
+        case 8:
+            if (gb == 8) return gram_dmma_kernel<8, 1, 1, 4, 4, 8>;
+            if (gb == 4) return gram_dmma_kernel<8, 1, 1, 4, 4, 4>;
+            if (gb == 2) return gram_dmma_kernel<8, 1, 1, 4, 4, 2>;
+            return gram_dmma_kernel<8, 1, 1, 4, 4, 1>;
+        case 16: {
+            const int v = g_gram16_variant >= 0 ? g_gram16_variant : (d >= 48 ? 0 : 3);
+            if (gb == 1) return gram_dmma_kernel<16, 2, 2, 4, 4, 1>;
+            if ((v == 1 || g_gram16_variant < 0) && gb == 2) return gram_dmma_kernel<16, 2, 2, 4, 4, 2>;
+            if (gb == 2) return gram_dmma_kernel<16, 2, 2, 4, 2, 2>;
+            if (v == 3 && gb == 4) return gram_dmma_kernel<16, 2, 2, 4, 1, 4>;
+            if (v == 5 && gb == 4) return gram_dmma_kernel<16, 2, 1, 2, 4, 4>;
+            if (v == 4 && gb == 4) return gram_dmma_kernel<16, 2, 2, 4, 4, 4>;
+            return gram_dmma_kernel<16, 2, 2, 4, 2, 4>;
+        }
+        case 32:
+            if (gb == 2) return gram_dmma_kernel<32, 4, 2, 2, 2, 2>;
+            return gram_dmma_kernel<32, 4, 2, 2, 4, 1>;
+        case 64:
+            return gram_dmma_kernel<64, 4, 4, 1, 2, 1>;
+        default:
+            return nullptr;
+    }
+}
+
+// Resident CTAs per SM of a Gram kernel (queried once per variant; 4 when no
+// device is present, e.g. host-only queries).
+int gram_occupancy(GramFn fn) {
+    static GramFn keys[64];
+    static int vals[64];
+    static int used = 0;
+    if (fn == nullptr) return 4;
+    for (int i = 0; i < used; ++i)
+        if (keys[i] == fn) return vals[i];
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kGramThreads, 0) != cudaSuccess ||
+        occ < 1) {
+        cudaGetLastError();
+        return 4;
+    }
+    if (used < 64) {
+        keys[used] = fn;
+        vals[used++] = occ;
+    }
+    return occ;
+}
+
+int gram_chunks(long long n, int d, int m1, int m2) {
+    int gb;
+    GramFn fn = select_gram(d, m1, m2, gb);
+    const long long groups = (d + gb - 1) / gb;
+    long long target = g_gram_target;
+    if (target <= 0) {
+        const long long waves = (m1 == 16 && m2 == 16 && d >= 48) ? 2 : 1;
+        target = 148LL * gram_occupancy(fn) * waves;
+    }
+    long long p = target / groups;  // floor: whole waves, no straggler CTAs
+    long long max_p = (n + 255) / 256;
+    if (p > max_p) p = max_p;
+    if (p < 1) p = 1;
+    return (int)p;
 }
 
 // Scalar Gram for arbitrary (m1, m2): thread (row-group, output) pairs.
@@ -283,6 +342,78 @@ update_dmma_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
                     long long r = rbase + 8 * mr + lc;
                     afr[mr] = (r < n) ? __ldg(Q + r * ldq + 4 * kk + lr) : 0.0;
                 }
+#pragma unroll
+                for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr], bfr[nt]);
+            }
+        }
+#pragma unroll
+        for (int mr = 0; mr < MR; ++mr) {
+            long long r = rbase + 8 * mr + lc;
+            if (r >= n) continue;
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                int b = 8 * nt + 2 * lr;
+                double o0 = sign * acc[mr][nt][0];
+                double o1 = sign * acc[mr][nt][1];
+                if (beta != 0.0) {
+                    o0 = beta * Win[r * ldwi + b] + o0;
+                    o1 = beta * Win[r * ldwi + b + 1] + o1;
+                }
+                Wout[r * ldwo + b] = o0;
+                Wout[r * ldwo + b + 1] = o1;
+            }
+        }
+    }
+}
+
+// Wide-block variant (M >= 32): the coefficient blocks C_i are staged once per
+// CTA in shared memory (rows padded to M + 4 doubles so the 4 k-rows of a
+// fragment fall 8 banks apart) and B fragments come from smem; 8 warps per
+// CTA, each walking its own 8*MR-row tiles (no block barriers in the loop).
+template <int M, int MR>
+__global__ void __launch_bounds__(256)
+update_smem_kernel(const double* const* __restrict__ Qs, int ldq, int d, const double* __restrict__ C,
+                   const double* Win, int ldwi, double* Wout, int ldwo, double beta, double sign,
+                   long long n, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    extern __shared__ double cs[];
+    constexpr int NT = M / 8;
+    constexpr int KK = M / 4;
+    constexpr int LDC = M + 4;
+    for (int e = threadIdx.x; e < d * M * M; e += blockDim.x) {
+        const int i = e / (M * M), rem = e % (M * M);
+        cs[(i * M + rem / M) * LDC + rem % M] = C[e];
+    }
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int lr = lane & 3;
+    const int lc = lane >> 2;
+    const long long warps_total = (long long)gridDim.x * (blockDim.x >> 5);
+    const long long tiles = (n + 8 * MR - 1) / (8 * MR);
+    for (long long tile = blockIdx.x * (long long)(blockDim.x >> 5) + (threadIdx.x >> 5); tile < tiles;
+         tile += warps_total) {
+        const long long rbase = tile * 8 * MR;
+        double acc[MR][NT][2];
+#pragma unroll
+        for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) acc[mr][nt][0] = acc[mr][nt][1] = 0.0;
+        for (int i = 0; i < d; ++i) {
+            const double* __restrict__ Q = Qs[i];
+            const double* Ci = cs + i * M * LDC;
+#pragma unroll 4
+            for (int kk = 0; kk < KK; ++kk) {
+                double afr[MR];
+#pragma unroll
+                for (int mr = 0; mr < MR; ++mr) {
+                    long long r = rbase + 8 * mr + lc;
+                    afr[mr] = (r < n) ? __ldg(Q + r * ldq + 4 * kk + lr) : 0.0;
+                }
+                double bfr[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) bfr[nt] = Ci[(4 * kk + lr) * LDC + 8 * nt + lc];
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr)
 #pragma unroll
@@ -462,29 +593,12 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     const int chunks = gram_chunks(n, d, m1, m2);
     const long long rc = rows_per_chunk(n, chunks);
     const int gb = gram_blocks_per_cta(d, m1, m2);
-    dim3 grid(chunks, (d + gb - 1) / gb);
+    dim3 grid(chunks, (d + gb - 1) / gb);  // generic kernel: gb == 1
     cudaStream_t st = as_stream(stream);
-#define GRAM_LAUNCH(M, TA, TB, KS, U, GB) \
-    gram_dmma_kernel<M, TA, TB, KS, U, GB><<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live)
-    if (m1 == m2 && m1 == 8) {
-        if (gb == 8) GRAM_LAUNCH(8, 1, 1, 4, 4, 8);
-        else if (gb == 4) GRAM_LAUNCH(8, 1, 1, 4, 4, 4);
-        else if (gb == 2) GRAM_LAUNCH(8, 1, 1, 4, 4, 2);
-        else GRAM_LAUNCH(8, 1, 1, 4, 4, 1);
-    } else if (m1 == m2 && m1 == 16) {
-        const int v = g_gram16_variant >= 0 ? g_gram16_variant : (d >= 48 ? 0 : 3);
-        if (gb == 1) GRAM_LAUNCH(16, 2, 2, 4, 4, 1);
-        else if ((v == 1 || g_gram16_variant < 0) && gb == 2) GRAM_LAUNCH(16, 2, 2, 4, 4, 2);
-        else if (gb == 2) GRAM_LAUNCH(16, 2, 2, 4, 2, 2);
-        else if (v == 3 && gb == 4) GRAM_LAUNCH(16, 2, 2, 4, 1, 4);
-        else if (v == 5 && gb == 4) GRAM_LAUNCH(16, 2, 1, 2, 4, 4);
-        else if (v == 4 && gb == 4) GRAM_LAUNCH(16, 2, 2, 4, 4, 4);
-        else GRAM_LAUNCH(16, 2, 2, 4, 2, 4);
-    } else if (m1 == m2 && m1 == 32) {
-        if (gb == 2) GRAM_LAUNCH(32, 4, 2, 2, 2, 2);
-        else GRAM_LAUNCH(32, 4, 2, 2, 4, 1);
-    } else if (m1 == m2 && m1 == 64) {
-        GRAM_LAUNCH(64, 4, 4, 1, 2, 1);
+    int gbs;
+    GramFn fn = select_gram(d, m1, m2, gbs);
+    if (fn != nullptr) {
+        fn<<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else {
         const int O = m1 * m2;
         size_t smem = (O <= 256) ? sizeof(double) * 256 : 0;
@@ -523,6 +637,20 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
     } else if (m1 == m2 && even && m1 == 16) {
         update_dmma_kernel<16, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
+    } else if (m1 == m2 && even && (m1 == 32 || m1 == 64) && (size_t)d * m1 * (m1 + 4) * 8 <= 200 * 1024) {
+        const size_t smem = (size_t)d * m1 * (m1 + 4) * sizeof(double);
+        const int mr = (m1 == 32) ? 4 : 2;
+        long long tiles = (n + 8 * mr - 1) / (8 * mr);
+        unsigned grid = grid_for(tiles, 8, 148LL * 8);
+        if (m1 == 32) {
+            auto fn = update_smem_kernel<32, 4>;
+            cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            fn<<<grid, 256, smem, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
+        } else {
+            auto fn = update_smem_kernel<64, 2>;
+            cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            fn<<<grid, 256, smem, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
+        }
     } else if (m1 == m2 && even && m1 == 32) {
         update_dmma_kernel<32, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);

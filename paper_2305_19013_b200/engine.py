@@ -273,6 +273,7 @@ class DeviceEngine:
         t = self.t_cur
         m = self.s * t
         d = len(self.retained)
+        self._cur = (k, d, m)  # read by optional kernel timers
         groups = self._width_groups()
         newest = self.retained[-1] if self.retained else None
         blk = self._new_block(m)
@@ -404,6 +405,7 @@ class DeviceEngine:
         t = self.t_cur
         m = t
         d = len(self.retained)
+        self._cur = (k, d, m)
         blk = self._new_block(m)
         WA, WC = self.WA.data_ptr(), self.WC.data_ptr()
         ptrs = [b.q.data_ptr() for b in self.retained] + [WA, WC, blk.q.data_ptr()]

@@ -155,6 +155,7 @@ class ShardedEngine(DeviceEngine):
         t = self.t_cur
         m = self.s * t
         d = len(self.retained)
+        self._cur = (k, d, m)
         newest = self.retained[-1] if self.retained else None
         blk = self._new_block(m)
         lWA, lWB = self._lptr(self.WA, m), self._lptr(self.WB, m)

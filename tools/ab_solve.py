@@ -23,13 +23,14 @@ for name, fuse in variants:
             if fuse is not None:
                 eng.fuse = fuse
             eng.kernel_timer = timer
+            timer.engine = eng
             timer.enabled = timed
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             x, r = eng.solve(b)
             e1.record(); e1.synchronize()
-            timer.harvest()
+            timer.harvest(r.iterations)
             ms.append(e0.elapsed_time(e1))
-        print(f"fuse={name} timed={timed}: iters={r.iterations} ms={[round(v,1) for v in ms]} timer={ {k: round(v,1) for k,v in timer.totals_ms().items()} }", flush=True)
-        timer.ms = {k: 0.0 for k in timer.ms}; timer.n = {k: 0 for k in timer.n}
+        print(f"fuse={name} timed={timed}: iters={r.iterations} ms={[round(v,1) for v in ms]} timer_records={len(timer.records)}", flush=True)
+        timer.records = []

@@ -4,5 +4,5 @@ timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/
 python -c "
 import json; d=json.load(open('gpurun_out/bench.json')); r=d['roofline']
 print('value', round(d['value'],1), 'ms/step', round(d['ms_per_step'],1), 'e2e', d['e2e'] and round(d['e2e']['value'],1))
-print('roofline', r['kernel'], round(r['achieved']), round(r['frac'],3), r['kernel_ms_total'], 'step_frac', round(r['step_model_frac'],3), 'clocks', d['clocks'])
+print('roofline', r['kernel'], round(r['achieved']), round(r['frac'],3), r['per_kernel'], 'step_frac', round(r['step_model_frac'],3), 'clocks', d['clocks'])
 "

@@ -1,0 +1,71 @@
+"""Event-timed kernel sweep at config sizes: Gram, block update, stencil, fused stencil kernels.
+
+    python tools/kernel_times.py [m n d ...]
+"""
+import json
+import sys
+
+import torch
+
+sys.path.insert(0, ".")
+from paper_2305_19013_b200 import _lib  # noqa: E402
+from paper_2305_19013_b200.operators import StencilOperator  # noqa: E402
+
+dev = "cuda"
+st = torch.cuda.current_stream().cuda_stream
+DMMA_TF = 37.1e12
+HBM = 6555.5e9
+
+
+def timeit(fn, reps=5):
+    for _ in range(2):
+        fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    e1.synchronize()
+    return e0.elapsed_time(e1) / reps / 1e3
+
+
+def sweep(m, shape, d):
+    n = 1
+    for s in shape:
+        n *= s
+    out = {}
+    Xs = [torch.randn(n * m, dtype=torch.float64, device=dev) for _ in range(d)]
+    Y = torch.randn(n * m, dtype=torch.float64, device=dev)
+    W = torch.randn(n * m, dtype=torch.float64, device=dev)
+    tab = torch.tensor([x.data_ptr() for x in Xs], dtype=torch.int64, device=dev)
+    chunks = _lib.query("ekcg_gram_chunks", n, d, m, m)
+    part = torch.empty(max(chunks * d * m * m, 1 << 20), dtype=torch.float64, device=dev)
+    C = torch.randn(d * m * m, dtype=torch.float64, device=dev) * 0.01
+    g = timeit(lambda: _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Y.data_ptr(), m, m, n, part.data_ptr(),
+                                 None, st))
+    out["gram"] = dict(s=g, GBs=8 * (d + 1) * n * m / g / 1e9, TF=2 * d * m * m * n / g / 1e12)
+    u = timeit(lambda: _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m,
+                                 W.data_ptr(), m, m, 1.0, -1.0, n, None, st))
+    out["update"] = dict(s=u, GBs=8 * (d + 2) * n * m / u / 1e9, TF=2 * d * m * m * n / u / 1e12)
+    op = StencilOperator(shape, 1.0)
+    Z = torch.empty_like(Y)
+    sp = timeit(lambda: op.apply(Y, m, Z, m, m))
+    out["stencil"] = dict(s=sp, GBs=16 * n * m / sp / 1e9)
+    for k, v in out.items():
+        v["hbm_frac"] = v["GBs"] * 1e9 / HBM
+        if "TF" in v:
+            v["fp64_frac"] = v["TF"] * 1e12 / DMMA_TF
+    return out
+
+
+if __name__ == "__main__":
+    cases = [(16, (64, 64, 64), 32), (16, (64, 64, 64), 110), (32, (128, 128, 128), 4), (64, (256, 256, 128), 3),
+             (64, (256, 256, 256), 2)]
+    res = {}
+    for m, shape, d in cases:
+        key = f"m{m}_n{'x'.join(map(str, shape))}_d{d}"
+        res[key] = sweep(m, shape, d)
+        print(key, json.dumps({k: {kk: round(vv, 4) for kk, vv in v.items()} for k, v in res[key].items()}),
+              flush=True)
+        torch.cuda.empty_cache()
+    json.dump(res, open("gpurun_out/kernel_times.json", "w"), indent=1)
