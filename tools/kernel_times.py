@@ -58,7 +58,7 @@ def sweep(m, shape, d):
     return out
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and "--fused" not in sys.argv:
     cases = [(16, (64, 64, 64), 32), (16, (64, 64, 64), 110), (32, (128, 128, 128), 4), (64, (256, 256, 128), 3),
              (64, (256, 256, 256), 2)]
     res = {}
@@ -69,3 +69,39 @@ if __name__ == "__main__":
               flush=True)
         torch.cuda.empty_cache()
     json.dump(res, open("gpurun_out/kernel_times.json", "w"), indent=1)
+
+
+def fused_times():
+    """Fused stencil kernels at config sizes (one call each, event timed)."""
+    from paper_2305_19013_b200.operators import StencilOperator as SO
+    import ctypes
+    res = {}
+    for m, shape in ((16, (64, 64, 64)), (32, (128, 128, 128)), (64, (256, 256, 128))):
+        n = shape[0] * shape[1] * shape[2]
+        op = SO(shape, 1.0)
+        X = torch.randn(n * m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        x = torch.zeros(n, dtype=torch.float64, device=dev)
+        r = torch.randn(n, dtype=torch.float64, device=dev)
+        alpha = torch.randn(m, dtype=torch.float64, device=dev) * 1e-3
+        part = torch.empty(_lib.query("ekcg_fused_partials", n, m), dtype=torch.float64, device=dev)
+        cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+        ctrl = torch.zeros(_lib.query("ekcg_ctrl_bytes"), dtype=torch.uint8, device=dev)
+        ctrl[0] = 1
+        G = torch.empty(m * m, dtype=torch.float64, device=dev)
+        hist = torch.zeros(16, dtype=torch.float64, device=dev)
+        rho2 = torch.zeros(1, dtype=torch.float64, device=dev)
+        tg = timeit(lambda: _lib.call("ekcg_stencil_cholinv", op.desc_ref(), X.data_ptr(), m, m, part.data_ptr(),
+                                      cnt.data_ptr(), G.data_ptr(), ctrl.data_ptr(), 1, 1e-14, 0, st))
+        tx = timeit(lambda: _lib.call("ekcg_stencil_xr", op.desc_ref(), X.data_ptr(), m, Y.data_ptr(), m, m,
+                                      alpha.data_ptr(), x.data_ptr(), r.data_ptr(), part.data_ptr(), cnt.data_ptr(),
+                                      ctrl.data_ptr(), 1, 10 ** 9, 0, hist.data_ptr(), 0, rho2.data_ptr(), st))
+        ts = timeit(lambda: op.apply(X, m, Y, m, m))
+        res[f"m{m}"] = {"stencil_cholinv_GBs": 8 * n * m / tg / 1e9, "stencil_xr_GBs": (16 * n * m + 32 * n) / tx / 1e9,
+                        "stencil_GBs": 16 * n * m / ts / 1e9}
+        print(f"m{m}", {k: round(v) for k, v in res[f"m{m}"].items()}, flush=True)
+    return res
+
+
+if __name__ == "__main__" and "--fused" in sys.argv:
+    fused_times()
