@@ -45,6 +45,7 @@ def parse():
     ap.add_argument("--cpu-iters", type=int, default=None, help="iterations in the CPU baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-timer", action="store_true", help="skip the per-kernel CUDA events")
     return ap.parse_args()
 
 
@@ -65,53 +66,58 @@ def peaks():
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    """SM clock and throttle reasons sampled with NVML from a background thread
+    during the timed region (every 100 ms; NVML calls release the GIL).  An
+    `nvidia-smi -lms` child at 100 ms was measured to slow kernel launches."""
 
-    def __init__(self, index):
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index, interval=0.1):
         self.index = index
-        self.rows = []
-        self.proc = None
+        self.interval = interval
+        self.samples = []
+        self.stop_evt = threading.Event()
+        self.thread = None
+        self.ok = False
 
     def start(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
-            self.thread.start()
-        except OSError:
-            self.proc = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception:
+            return
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.thread.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) >= 7:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nvml
+        while not self.stop_evt.is_set():
+            try:
+                mhz = nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksThrottleReasons(self.handle)
+                self.samples.append((mhz, rs))
+            except Exception:
+                pass
+            self.stop_evt.wait(self.interval)
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=2)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons, sm, smax = set(), [], []
-        for r in self.rows:
-            try:
-                sm.append(float(r[0]))
-                smax.append(float(r[1]))
-            except ValueError:
-                continue
-            for name, flag in zip(names, r[3:7]):
-                if flag.lower() == "active":
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        self.stop_evt.set()
+        self.thread.join(2)
+        reasons = set()
+        for _, rs in self.samples:
+            for name, bit in self.REASONS.items():
+                if rs & bit:
                     reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+        mhz = [s[0] for s in self.samples]
+        return {"sm_mhz": statistics.median(mhz) if mhz else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(mhz), "source": "nvml"}
 
 
 # ---------------------------------------------------------------------------
@@ -244,7 +250,7 @@ def run_ours(args):
             eng = DeviceEngine(op, prob.partition, cfg, device=dev)
         eng.kernel_timer = timer
         timer.engine = eng
-        timer.enabled = timed
+        timer.enabled = timed and not args.no_kernel_timer
         x, rep = eng.solve(b_dev)
         return rep, eng
 
