@@ -316,14 +316,17 @@ def run_ours(args):
     hbm, peak_kind = peaks()
     achieved = per_tag[dom][0] / (per_tag[dom][2] / 1e3) / 1e9 if dom else None
     prof = ROOT / "profiles" / "r01_traffic.json"
-    traffic = None
+    traffic, traffic_alg, traffic_d = None, None, None
     if prof.exists() and dom:
-        traffic = json.loads(prof.read_text()).get(dom)
+        tr = json.loads(prof.read_text())
+        traffic, traffic_alg, traffic_d = tr.get(dom), tr.get(dom + "_alg"), tr.get(dom + "_d")
     model_bytes = sum(r.model_bytes for r in reps)
     model_time = model_bytes / (hbm * 1e9)
     roofline = {
         "bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
         "frac": (achieved / hbm) if achieved else None, "traffic": traffic, "kernel": dom,
+        "traffic_alg_bytes": traffic_alg, "traffic_launch_d": traffic_d,
+        "traffic_source": "profiles/r01_traffic.json (ncu --set full, one launch)",
         "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)",
         "per_kernel": {t: {"GBs": v[0] / (v[2] / 1e3) / 1e9, "TFLOPs": v[1] / (v[2] / 1e3) / 1e12,
                            "ms_total": round(v[2], 3), "launches": v[3]} for t, v in per_tag.items()},
