@@ -173,7 +173,10 @@ int ekcg_ctrl_bytes(void);
 int ekcg_start(void* ctrl, const double* rho2, double tol, double* history, void* stream);
 
 /* End of iteration k: rho = sqrt(*rho2), history[k] = rho, stagnation guard
- * (window > 0), convergence (rho <= tol*rho0) and kmax checks (solvers.py:357,399,406-415). */
+ * (window > 0), convergence (rho <= tol*rho0) and kmax checks (solvers.py:357,399,406-415).
+ * Everywhere an iteration number is passed (k / iteration arguments of the
+ * finish, factor and fused kernels), k <= 0 means "read it on the device as
+ * ctrl->k_done + 1" -- what CUDA-graph replay of an iteration uses. */
 int ekcg_finish(void* ctrl, const double* rho2, int k, int kmax, int stagnation_window,
                 double* history, void* stream);
 

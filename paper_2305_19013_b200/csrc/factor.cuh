@@ -77,6 +77,7 @@ __device__ inline void tri_inverse(const double* R, double* S, int m) {
 }
 
 __device__ inline void record_breakdown(EkcgCtrl* ctrl, int kind, int col, double piv, double scale, int iteration) {
+    if (iteration <= 0) iteration = ctrl->k_done + 1;  // graph replay: iteration read on the device
     ctrl->brk_kind = kind;
     ctrl->brk_col = col;
     ctrl->brk_pivot = piv;
@@ -150,6 +151,7 @@ __device__ inline void cholinv_body(double* G, double* R, double* S, int m, doub
 // End of iteration k (solvers.py:398-415, :357), single thread.
 __device__ inline void finish_body(EkcgCtrl* ctrl, double rho2, int k, int kmax, int stagnation_window,
                                    double* history) {
+    if (k <= 0) k = ctrl->k_done + 1;  // graph replay: iteration read on the device
     double rho = sqrt(rho2);
     history[k] = rho;
     ctrl->k_done = k;

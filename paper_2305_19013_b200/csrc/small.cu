@@ -143,7 +143,7 @@ extern "C" int ekcg_start(void* ctrl, const double* rho2, double tol, double* hi
 
 extern "C" int ekcg_finish(void* ctrl, const double* rho2, int k, int kmax, int stagnation_window,
                            double* history, void* stream) {
-    if (ctrl == nullptr || k < 1) return EKCG_EINVAL;
+    if (ctrl == nullptr) return EKCG_EINVAL;
     finish_kernel<<<1, 1, 0, as_stream(stream)>>>((EkcgCtrl*)ctrl, rho2, k, kmax, stagnation_window, history);
     ++g_ekcg_launches;
     return launch_status();

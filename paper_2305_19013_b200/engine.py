@@ -47,6 +47,7 @@ class _PtrArena:
         self._alloc(capacity)
 
     def _alloc(self, cap):
+        self.floor = 0  # regions below `floor` belong to captured CUDA graphs
         self.cap = cap
         self.host = torch.empty(cap, dtype=torch.int64, pin_memory=True)
         self.hnp = self.host.numpy()
@@ -57,9 +58,9 @@ class _PtrArena:
         L = len(ptrs)
         if self.cur + L > self.cap:
             torch.cuda.current_stream(self.device).synchronize()
-            if L > self.cap:
-                self._alloc(2 * L)
-            self.cur = 0
+            if self.floor + L > self.cap:
+                raise RuntimeError("pointer arena exhausted by captured graphs")
+            self.cur = self.floor
         s = self.cur
         self.hnp[s:s + L] = ptrs
         self.dev[s:s + L].copy_(self.host[s:s + L], non_blocking=True)
@@ -103,6 +104,12 @@ class DeviceEngine:
         # blocks of HBM instead of 2w + 3; two extra operator applications per
         # iteration).  "auto" picks lean only when the cached scheme does not fit.
         self.cache_aq = "auto"
+        # replay steady-state iterations of truncated windows from CUDA graphs
+        # (one per ring phase; iteration numbers are read on the device).  Off by
+        # default: measured on config 1, capture costs more than the direct
+        # launches it replaces (15 ms per 130-iteration solve without graphs).
+        self.use_graphs = False
+        self._capturing = False
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -133,8 +140,9 @@ class DeviceEngine:
         self.ctrl_host = torch.empty(self.ctrl.numel(), dtype=torch.uint8, pin_memory=True)
         self.snap_bufs = [torch.empty(self.ctrl.numel(), dtype=torch.uint8, pin_memory=True) for _ in range(3)]
         self.live = self.ctrl.data_ptr()
-        self.history = torch.zeros(min(self.kmax, 4096) + 1, **f64)
-        self.checks = torch.zeros(max(1, min(self.kmax, 4096) // self.every + 1), **f64)
+        hist_len = min(self.kmax, 1 << 20) + 1 if self.window is not None else min(self.kmax, 4096) + 1
+        self.history = torch.zeros(hist_len, **f64)
+        self.checks = torch.zeros(max(1, (hist_len - 1) // self.every + 1), **f64)
         self.arena = _PtrArena(dev)
         self.owner_dev = self.partition.device_owner(dev)
         self.part_obj = self.partition
@@ -173,6 +181,47 @@ class DeviceEngine:
             buf = torch.empty(max(numel, 2 * buf.numel()), dtype=buf.dtype, device=self.device)
             setattr(self, name, buf)
         return buf
+
+    def _karg(self, k):
+        """Iteration number as a kernel argument: <= 0 inside a graph capture
+        (the kernels then read ctrl->k_done + 1 on the device)."""
+        return -1 if self._capturing else k
+
+    def _graph_eligible(self):
+        return (self.use_graphs and self.kernel_timer is None and self.window is not None
+                and self.retention == "trunc" and self.cfg.switch_tol is None
+                and self.method in ("sre-cg2", "sre-cg") and self.kmax + 1 <= self.history.numel())
+
+    def _host_step(self, k):
+        """Host bookkeeping of a replayed iteration (what _enqueue_iteration does besides launching)."""
+        m = self.s * self.t_cur
+        d = len(self.retained)
+        self._cur = (k, d, m)
+        blk = self._new_block(m)
+        self._append(blk)
+        self._account(k, d, m, False, self.t_cur)
+
+    def _capture_iteration(self, k):
+        """Capture iteration k (a steady-state ring phase) into a CUDA graph; returns it (not yet replayed)."""
+        g = torch.cuda.CUDAGraph()
+        m, d = self.s * self.t_cur, len(self.retained)
+        self._ensure("part", max(self.fused_part, self._chunks(d, m, m) * d * m * m, self._chunks(1, m, m) * m * m,
+                                 self._chunks(1, m, 1) * m, self._chunks(1, m, m) * m * m))
+        self._ensure("C", d * m * m + 1)
+        if self.arena.cur + 4 * (2 * d + 8) > self.arena.cap:  # never wrap while capturing
+            torch.cuda.current_stream(self.device).synchronize()
+            self.arena.cur = self.arena.floor
+        saved = self.stream
+        self._capturing = True
+        try:
+            with torch.cuda.graph(g):
+                self.stream = torch.cuda.current_stream(self.device).cuda_stream
+                self._enqueue_iteration(k, 1.0)
+        finally:
+            self._capturing = False
+            self.stream = saved
+        self.arena.floor = self.arena.cur
+        return g
 
     def _chunks(self, d, m1, m2):
         key = (d, m1, m2)
@@ -322,7 +371,7 @@ class DeviceEngine:
                     # W'' = W' - Q C2 fused with Graw = W''^T W'' and the Pre-CholQR factor
                     self._timed("hist_update", lambda: _lib.call(
                         "ekcg_update_prechol", q_addr(0), m, d, C.data_ptr(), WA, m, WA, m, m, n,
-                        part.data_ptr(), self.counter.data_ptr(), self.S0.data_ptr(), live, k, 1e-14, st))
+                        part.data_ptr(), self.counter.data_ptr(), self.S0.data_ptr(), live, self._karg(k), 1e-14, st))
                     have_s0 = True
                     break
                 off = 0
@@ -337,18 +386,18 @@ class DeviceEngine:
         # ---- Pre-CholQR (aortho.py:98-110) ----
         if not have_s0:
             self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
-            _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+            _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, self._karg(k), 1e-14, st)
         self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WB, m, m, 0.0, 1.0, tag="tri_apply")
         finish_now = (k % self.every != 0)
         if fused and "cholinv" in self.fuse:
             # G = W0^T A W0 (A W0 never written) + A-CholQR factor S
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WB, m, m, part.data_ptr(), self.counter.data_ptr(),
-                self.S.data_ptr(), live, k, 1e-14, 1, st))
+                self.S.data_ptr(), live, self._karg(k), 1e-14, 1, st))
         else:
             self._apply_op(WB, m, WC, m, m)
             self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_self")
-            _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+            _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, self._karg(k), 1e-14, st)
         if fused and "vec" in self.fuse:
             # W_k = W0 S + alpha = W_k^T r
             self._timed("tri_alpha", lambda: _lib.call(
@@ -365,7 +414,7 @@ class DeviceEngine:
             self._timed("spmm_xr", lambda: _lib.call(
                 "ekcg_stencil_xr", self.op.desc_ref(), blk.q.data_ptr(), m, blk.aq.data_ptr(), m, m,
                 self.alpha.data_ptr(), self.x.data_ptr(), self.r.data_ptr(), part.data_ptr(),
-                self.counter.data_ptr(), live, k, self.kmax, self.stag_window, self.history.data_ptr(),
+                self.counter.data_ptr(), live, self._karg(k), self.kmax, self.stag_window, self.history.data_ptr(),
                 1 if finish_now else 0, self.rho2.data_ptr(), st))
         else:
             self._apply_op(blk.q.data_ptr(), m, blk.aq.data_ptr(), m, m)
@@ -382,7 +431,7 @@ class DeviceEngine:
             _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
         if not (xr_fused and finish_now):
             self._ensure_history(k + 1)
-            _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+            _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), self._karg(k), self.kmax, self.stag_window,
                       self.history.data_ptr(), st)
         self._account(k, d, m, fresh, t)
 
@@ -424,19 +473,19 @@ class DeviceEngine:
                 self._gram(q_addr(0), m, d, m, WC, m, m, C.data_ptr(), tag="hist_gram")
                 self._update(q_addr(0), m, d, m, C.data_ptr(), WA, m, WA, m, m, 1.0, -1.0, tag="hist_update")
         self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
-        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, self._karg(k), 1e-14, st)
         self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WC, m, m, 0.0, 1.0, tag="tri_apply")  # W0 -> WC
         if fused:
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WC, m, m, part.data_ptr(), self.counter.data_ptr(),
-                self.S.data_ptr(), live, k, 1e-14, 1, st))
+                self.S.data_ptr(), live, self._karg(k), 1e-14, 1, st))
             self._timed("tri_alpha", lambda: _lib.call(
                 "ekcg_update_vec", WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
                 part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
         else:
             self._apply_op(WC, m, WA, m, m)  # A W0 -> WA (free)
             self._gram(WC_arr, m, 1, m, WA, m, m, self.G.data_ptr(), tag="gram_self")
-            _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+            _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, self._karg(k), 1e-14, st)
             self._update(WC_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
                          tag="tri_apply")
             self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
@@ -446,7 +495,7 @@ class DeviceEngine:
             self._timed("spmm_xr", lambda: _lib.call(
                 "ekcg_stencil_xr", self.op.desc_ref(), blk.q.data_ptr(), m, WA, m, m,
                 self.alpha.data_ptr(), self.x.data_ptr(), self.r.data_ptr(), part.data_ptr(),
-                self.counter.data_ptr(), live, k, self.kmax, self.stag_window, self.history.data_ptr(),
+                self.counter.data_ptr(), live, self._karg(k), self.kmax, self.stag_window, self.history.data_ptr(),
                 1 if finish_now else 0, self.rho2.data_ptr(), st))
         else:
             self._apply_op(blk.q.data_ptr(), m, WA, m, m)  # A W_k -> WA: next candidate
@@ -462,7 +511,7 @@ class DeviceEngine:
             _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
         if not (fused and finish_now):
             self._ensure_history(k + 1)
-            _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+            _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), self._karg(k), self.kmax, self.stag_window,
                       self.history.data_ptr(), st)
         self._account(k, d, m, fresh, t)
 
@@ -555,6 +604,8 @@ class DeviceEngine:
         tol1 = 1.0
         ctrl = None
         snaps = []
+        graphs = {} if (not sync_each and self._graph_eligible()) else None
+        self._graphs = graphs
         while k <= self.kmax:
             if sync_each:
                 self._enqueue_iteration(k, tol1)
@@ -575,7 +626,18 @@ class DeviceEngine:
                 for _ in range(lookahead):
                     if k > self.kmax:
                         break
-                    self._enqueue_iteration(k, 1.0)
+                    w = self.window
+                    if (graphs is not None and k > 2 * w and k % self.every != 0
+                            and len(self.retained) == w):
+                        phase = (k - 1) % w
+                        g = graphs.get(phase)
+                        if g is None:  # first visit of this phase in steady state: capture
+                            g = graphs[phase] = self._capture_iteration(k)
+                        else:
+                            self._host_step(k)
+                        g.replay()
+                    else:
+                        self._enqueue_iteration(k, 1.0)
                     k += 1
                 snaps.append(self._snapshot(len(snaps)))
                 if len(snaps) >= 2:

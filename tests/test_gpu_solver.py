@@ -306,3 +306,26 @@ def test_sharded_engine_single_rank_matches(idx, edge, over):
     assert rep.restart_iterations == ref.restart_iterations
     assert abs(rep.true_residual - ref.true_residual) <= 1e-6 * ref.true_residual + 1e-300
     assert x.shape == (prob.n,)
+
+
+@pytest.mark.parametrize("idx,edge", [(1, 100), (3, 16), (4, 10), (5, 64)])
+def test_graph_replay_matches_direct_launches(idx, edge):
+    """Steady-state iterations of truncated windows replayed from CUDA graphs
+    (iteration number read on the device) equal the directly launched ones bitwise."""
+    from paper_2305_19013_b200.engine import DeviceEngine
+    prob = make_config(idx, edge)
+    cfg = SolverConfig(**dict(prob.solver_kwargs, kmax=min(300, 10 * prob.n)))
+    op = prob.stencil()
+    reps = []
+    for graphs in (True, False):
+        eng = DeviceEngine(op, prob.partition, cfg)
+        eng.use_graphs = graphs
+        x, rep = eng.solve(prob.b)
+        reps.append((x, rep, eng))
+    (xa, a, ea), (xb, b, eb) = reps
+    assert ea._graphs, "graph mode was not used"
+    assert a.iterations == b.iterations and a.status == b.status
+    assert np.array_equal(a.residual_history, b.residual_history)
+    assert np.array_equal(xa, xb)
+    assert a.peak_block_vectors == b.peak_block_vectors
+    assert [c[0] for c in a.true_residual_checks] == [c[0] for c in b.true_residual_checks]
