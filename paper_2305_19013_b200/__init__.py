@@ -26,6 +26,7 @@ from .solvers import (
     SolverConfig,
     enlarged_solve,
 )
+from .reporting import CSV_COLUMNS, make_rhs, run_batch, write_history, write_runs_csv
 from .problems import (
     box_partition,
     diffusion_csr,
@@ -66,4 +67,9 @@ __all__ = [
     "gen_skyscraper",
     "box_partition",
     "make_config",
+    "make_rhs",
+    "run_batch",
+    "write_history",
+    "write_runs_csv",
+    "CSV_COLUMNS",
 ]
