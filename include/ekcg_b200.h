@@ -57,6 +57,11 @@ int ekcg_split_axpy(const double* v, const int* owner, const double* Wprev, int 
                     const double* beta, double beta_sign, double* W, long long n, int t, int ldw,
                     const int* live, void* stream);
 
+/* W[:, j] += Wprev[:, j] * beta_sign * beta[j] ; the preconditioned MSDO-CG
+ * candidate (solvers.py:378-382) once W holds M^-1 split(r). */
+int ekcg_axpy_cols(double* W, int ldw, const double* Wprev, int ldp, const double* beta, double beta_sign,
+                   long long n, int t, const int* live, void* stream);
+
 /* Y = A X for CSR A (int64 row_ptr, int32 col_idx) ; replaces spmm/spmv
  * (linalg.py:133-152).  Bit-exact with numpy's reduceat association. */
 int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const double* values,
@@ -101,6 +106,22 @@ int ekcg_xr_update(const double* W, int ldw, const double* AW, int ldaw, const d
 
 /* partials[p] = partial sum of v^2 (ekcg_vec_chunks(n) partials). */
 int ekcg_sumsq(const double* v, long long n, double* partials, const int* live, void* stream);
+
+/* Block-diagonal dense product Y = B X (Y != X) over consecutive row blocks:
+ * block b covers rows [starts[b], starts[b+1]), its dense nb x nb row-major
+ * lower-triangular matrix sits at data[offs[b]]; transpose = 1 applies B_b^T.
+ * row_block[i] is the block of row i.  With B = L^-1 / L this is the
+ * block-Jacobi forward_solve / backward_solve / mult_l / mult_lt of
+ * blockjacobi.py:145-170 (inverse factors precomputed at setup). */
+int ekcg_block_diag_apply(const double* data, const long long* offs, const int* starts, const int* row_block,
+                          int transpose, const double* X, int ldx, double* Y, int ldy, long long n, int m,
+                          const int* live, void* stream);
+
+/* Block-diagonal triangular solves by substitution, one thread per (block,
+ * column): L_b Y_b = X_b (transpose = 0) or L_b^T Y_b = X_b (transpose = 1),
+ * the solve_triangular calls of blockjacobi.py:145-152.  Y may alias X. */
+int ekcg_block_trsv(const double* L, const long long* offs, const int* starts, int nblocks, int transpose,
+                    const double* X, int ldx, double* Y, int ldy, int m, const int* live, void* stream);
 
 /* dst[i, 0:w] = src[i, 0:w] for i < n (row strides lds, ldd): the s-step
  * chain seed V1 = newest t columns of the cached A W (solvers.py:338-339). */

@@ -26,6 +26,15 @@ from .solvers import (
     SolverConfig,
     enlarged_solve,
 )
+from .precond import (
+    BlockJacobiFactor,
+    aligned_with,
+    apply_minv,
+    backward_solve,
+    build_block_jacobi,
+    forward_solve,
+    uniform_block_bounds,
+)
 from .reporting import CSV_COLUMNS, make_rhs, run_batch, write_history, write_runs_csv
 from .problems import (
     box_partition,
@@ -72,4 +81,11 @@ __all__ = [
     "write_history",
     "write_runs_csv",
     "CSV_COLUMNS",
+    "BlockJacobiFactor",
+    "uniform_block_bounds",
+    "build_block_jacobi",
+    "forward_solve",
+    "backward_solve",
+    "apply_minv",
+    "aligned_with",
 ]

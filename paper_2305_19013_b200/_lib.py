@@ -18,6 +18,8 @@ SIGNATURES = {
     "ekcg_split": (c_int, [c_void_p, c_void_p, c_void_p, c_longlong, c_int, c_int, c_void_p, c_void_p]),
     "ekcg_split_axpy": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_double, c_void_p,
                                 c_longlong, c_int, c_int, c_void_p, c_void_p]),
+    "ekcg_axpy_cols": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_double, c_longlong, c_int, c_void_p,
+                               c_void_p]),
     "ekcg_spmm_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_longlong,
                               c_int, c_void_p, c_void_p]),
     "ekcg_spmm_stencil": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p]),
@@ -31,6 +33,10 @@ SIGNATURES = {
     "ekcg_xr_update": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p,
                                c_longlong, c_void_p, c_void_p, c_void_p]),
     "ekcg_sumsq": (c_int, [c_void_p, c_longlong, c_void_p, c_void_p, c_void_p]),
+    "ekcg_block_diag_apply": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_void_p,
+                                      c_int, c_longlong, c_int, c_void_p, c_void_p]),
+    "ekcg_block_trsv": (c_int, [c_void_p, c_void_p, c_void_p, c_int, c_int, c_void_p, c_int, c_void_p, c_int,
+                                c_int, c_void_p, c_void_p]),
     "ekcg_copy_cols": (c_int, [c_void_p, c_int, c_void_p, c_int, c_longlong, c_int, c_void_p, c_void_p]),
     "ekcg_sub": (c_int, [c_void_p, c_void_p, c_void_p, c_longlong, c_void_p, c_void_p]),
     "ekcg_prechol": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int, c_double, c_void_p]),

@@ -545,6 +545,67 @@ sumsq_kernel(const double* __restrict__ v, long long n, double* __restrict__ par
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// Block-diagonal dense apply Y = B X over consecutive row blocks (block-Jacobi
+// preconditioner factors, blockjacobi.py:136-170): B_b is a dense nb x nb
+// row-major matrix at data[offs[b]]; mode 0: B_b lower, 1: B_b^T of a lower
+// matrix (upper), per row i of block b: y_ic = sum_j B_b[i][j] x_jc.
+__global__ void block_diag_apply_kernel(const double* __restrict__ data, const long long* __restrict__ offs,
+                                        const int* __restrict__ starts, const int* __restrict__ row_block,
+                                        int transpose, const double* __restrict__ X, int ldx,
+                                        double* __restrict__ Y, int ldy, long long n, int m,
+                                        const int* __restrict__ live) {
+    EKCG_GATE(live);
+    const long long total = n * (long long)m;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const long long i = e / m;
+        const int c = (int)(e - i * m);
+        const int b = row_block[i];
+        const int s0 = starts[b], nb = starts[b + 1] - s0;
+        const int li = (int)(i - s0);
+        const double* B = data + offs[b];
+        double acc = 0.0;
+        if (!transpose) {
+            for (int j = 0; j <= li; ++j) acc += B[li * nb + j] * X[(long long)(s0 + j) * ldx + c];
+        } else {
+            for (int j = li; j < nb; ++j) acc += B[j * nb + li] * X[(long long)(s0 + j) * ldx + c];
+        }
+        Y[i * ldy + c] = acc;
+    }
+}
+
+// Block-diagonal triangular solves by substitution, one thread per (block,
+// column): L_b y = x (forward) or L_b^T y = x (backward) -- the
+// solve_triangular calls of blockjacobi.py:145-152.  In place allowed.
+__global__ void block_trsv_kernel(const double* __restrict__ data, const long long* __restrict__ offs,
+                                  const int* __restrict__ starts, int nblocks, int transpose,
+                                  const double* X, int ldx, double* Y, int ldy, int m,
+                                  const int* __restrict__ live) {
+    EKCG_GATE(live);
+    const long long total = (long long)nblocks * m;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int b = (int)(e / m), c = (int)(e - (long long)b * m);
+        const int s0 = starts[b], nb = starts[b + 1] - s0;
+        const double* L = data + offs[b];
+        const double* x = X + (long long)s0 * ldx + c;
+        double* y = Y + (long long)s0 * ldy + c;
+        if (!transpose) {
+            for (int i = 0; i < nb; ++i) {
+                double acc = x[(long long)i * ldx];
+                for (int j = 0; j < i; ++j) acc -= L[i * nb + j] * y[(long long)j * ldy];
+                y[(long long)i * ldy] = acc / L[i * nb + i];
+            }
+        } else {
+            for (int i = nb - 1; i >= 0; --i) {
+                double acc = x[(long long)i * ldx];
+                for (int j = i + 1; j < nb; ++j) acc -= L[j * nb + i] * y[(long long)j * ldy];
+                y[(long long)i * ldy] = acc / L[i * nb + i];
+            }
+        }
+    }
+}
+
 __global__ void copy_cols_kernel(const double* __restrict__ src, int lds, double* __restrict__ dst, int ldd,
                                  long long n, int w, const int* __restrict__ live) {
     EKCG_GATE(live);
@@ -688,6 +749,27 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
 extern "C" int ekcg_sumsq(const double* v, long long n, double* partials, const int* live, void* stream) {
     if (n < 1) return EKCG_EINVAL;
     sumsq_kernel<<<vec_chunks(n), kVecThreads, 0, as_stream(stream)>>>(v, n, partials, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_block_diag_apply(const double* data, const long long* offs, const int* starts,
+                                     const int* row_block, int transpose, const double* X, int ldx, double* Y,
+                                     int ldy, long long n, int m, const int* live, void* stream) {
+    if (n < 1 || m < 1 || ldx < m || ldy < m || X == Y) return EKCG_EINVAL;
+    block_diag_apply_kernel<<<grid_for(n * m, 256), 256, 0, as_stream(stream)>>>(data, offs, starts, row_block,
+                                                                                 transpose, X, ldx, Y, ldy, n, m,
+                                                                                 live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_block_trsv(const double* L, const long long* offs, const int* starts, int nblocks,
+                               int transpose, const double* X, int ldx, double* Y, int ldy, int m,
+                               const int* live, void* stream) {
+    if (nblocks < 1 || m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
+    block_trsv_kernel<<<grid_for((long long)nblocks * m, 128), 128, 0, as_stream(stream)>>>(
+        L, offs, starts, nblocks, transpose, X, ldx, Y, ldy, m, live);
     ++g_ekcg_launches;
     return launch_status();
 }

@@ -67,6 +67,18 @@ __global__ void split_axpy_kernel(const double* __restrict__ v, const int* __res
     }
 }
 
+// W[i, j] += Wprev[i, j] * (beta_sign * beta[j])  (preconditioned MSDO candidate,
+// solvers.py:378-382 with candidate_split = M^-1 split(r) already in W)
+__global__ void axpy_cols_kernel(double* __restrict__ W, int ldw, const double* __restrict__ Wprev, int ldp,
+                                 const double* __restrict__ beta, double beta_sign, long long n, int t,
+                                 const int* __restrict__ live) {
+    EKCG_GATE(live);
+    ROW_LOOP(i, n) {
+        for (int j = threadIdx.x; j < t; j += blockDim.x)
+            W[i * ldw + j] = add_rn(W[i * ldw + j], mul_rn(Wprev[i * ldp + j], beta_sign * beta[j]));
+    }
+}
+
 // ---------------------------------------------------------------------------
 // numpy pairwise summation of the row tail p_1..p_cnt for one column.
 // ---------------------------------------------------------------------------
@@ -191,6 +203,16 @@ extern "C" int ekcg_split_axpy(const double* v, const int* owner, const double* 
     RowLaunch L = row_launch(n, t < 32 ? t : 32);
     split_axpy_kernel<<<L.grid, L.block, 0, as_stream(stream)>>>(v, owner, Wprev, ldp, beta, beta_sign, W, n, t,
                                                                  ldw, live);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
+extern "C" int ekcg_axpy_cols(double* W, int ldw, const double* Wprev, int ldp, const double* beta,
+                              double beta_sign, long long n, int t, const int* live, void* stream) {
+    if (n < 0 || t < 1 || ldw < t || ldp < t) return EKCG_EINVAL;
+    if (n == 0) return EKCG_OK;
+    RowLaunch L = row_launch(n, t < 32 ? t : 32);
+    axpy_cols_kernel<<<L.grid, L.block, 0, as_stream(stream)>>>(W, ldw, Wprev, ldp, beta, beta_sign, n, t, live);
     ++g_ekcg_launches;
     return launch_status();
 }

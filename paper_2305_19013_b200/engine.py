@@ -104,6 +104,19 @@ class DeviceEngine:
         # blocks of HBM instead of 2w + 3; two extra operator applications per
         # iteration).  "auto" picks lean only when the cached scheme does not fit.
         self.cache_aq = "auto"
+        # split block-Jacobi preconditioner, "modified" mode (solvers.py:326-339)
+        self.pc = None
+        self.pc_aligned = True
+        self.norm_pc = None  # explicit-hat mode: residual norms are |L r_hat| (solvers.py:305-306)
+        self.notes_init = []
+        F = cfg.preconditioner
+        if F is not None and cfg.precond_mode == "modified":
+            from .precond import DevicePreconditioner, aligned_with
+            self.pc = F if isinstance(F, DevicePreconditioner) else DevicePreconditioner(F, self.device)
+            self.pc_aligned = aligned_with(self.pc.host, partition)
+            if not self.pc_aligned:
+                self.notes_init.append("preconditioner blocks not aligned with partition subdomains; "
+                                       "using explicit split application")
         # replay steady-state iterations of truncated windows from CUDA graphs
         # (one per ring phase; iteration numbers are read on the device).  Off by
         # default: measured on config 1, capture costs more than the direct
@@ -124,6 +137,8 @@ class DeviceEngine:
         self.WB = torch.empty(0 if self.lean else n * mm, **f64)
         self.WC = torch.empty(n * mm, **f64)
         self.tmpv = torch.empty(n, **f64)
+        self.tmpv2 = torch.empty(n, **f64)
+        self.tmpv3 = torch.empty(n, **f64)
         self.Graw = torch.empty(mm * mm, **f64)
         self.G = torch.empty(mm * mm, **f64)
         self.S0 = torch.empty(mm * mm, **f64)
@@ -162,7 +177,7 @@ class DeviceEngine:
 
     def _choose_lean(self, n, m):
         eligible = (self.window is not None and self.s == 1 and self.method in ("sre-cg2", "sre-cg")
-                    and self.cfg.switch_tol is None)
+                    and self.cfg.switch_tol is None and self.pc is None)
         if self.cache_aq is True or not eligible:
             if self.cache_aq is False and not eligible:
                 raise ValueError("the lean (no A Q cache) scheme needs a truncation window, s = 1, "
@@ -337,21 +352,31 @@ class DeviceEngine:
         # ---- candidate block (solvers.py:366-382) ----
         fresh = switched or not self.retained
         W = WA
+        pc = self.pc
         if fresh or self.method == "modified-msdo-cg":
-            _lib.call("ekcg_split", self.r.data_ptr(), self.owner_dev.data_ptr(), WA, n, t, m, live, st)
+            self._candidate_split(WA, t, m)
             self._chain(WA, m, t)
         elif self.method in ("sre-cg2", "sre-cg"):
-            if self.s == 1:
+            if pc is not None:  # chain_next = M^-1 A W_{k-1} (solvers.py:338-339)
+                self._minv(newest.aq.data_ptr(), newest.width, WA, m, m)
+            elif self.s == 1:
                 W = newest.aq.data_ptr()  # W_k = A W_{k-1}: read the cached product in place
             else:
                 src = newest.aq.data_ptr() + F64 * (newest.width - t)
                 _lib.call("ekcg_copy_cols", src, newest.width, WA, m, n, t, live, st)
                 self._chain(WA, m, t)
-        else:  # msdo-cg: split(r) + W_prev diag(-(AW_prev^T r))
+        elif pc is None:  # msdo-cg: split(r) + W_prev diag(-(AW_prev^T r))
             self._gram(NEWEST_AQ_arr, newest.width, 1, newest.width, self.r.data_ptr(), 1, 1,
                        self.beta.data_ptr(), tag="gram_vec")
             _lib.call("ekcg_split_axpy", self.r.data_ptr(), self.owner_dev.data_ptr(), newest.q.data_ptr(),
                       newest.width, self.beta.data_ptr(), -1.0, WA, n, t, m, live, st)
+        else:  # preconditioned msdo-cg: M^-1 split(r) + W_prev diag(-(AW_prev^T M^-1 r))
+            self._minv(self.r.data_ptr(), 1, self.tmpv2.data_ptr(), 1, 1)
+            self._gram(NEWEST_AQ_arr, newest.width, 1, newest.width, self.tmpv2.data_ptr(), 1, 1,
+                       self.beta.data_ptr(), tag="gram_vec")
+            self._candidate_split(WA, t, m)
+            _lib.call("ekcg_axpy_cols", WA, m, newest.q.data_ptr(), newest.width, self.beta.data_ptr(), -1.0, n, t,
+                      live, st)
 
         fused = (self.fused_ok and m in (8, 16, 32, 64)
                  and all(b.width == m for b in self.retained))
@@ -423,6 +448,9 @@ class DeviceEngine:
                 "ekcg_xr_update", blk.q.data_ptr(), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
                 self.x.data_ptr(), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st))
             _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
+            if self.norm_pc is not None:  # |L r_hat| instead of |r_hat|
+                _lib.call("ekcg_sumsq", self._normed(self.r, live), n, self.vpart.data_ptr(), live, st)
+                _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
         self._append(blk)
         if not finish_now:  # true-residual drift log (solvers.py:401-402)
             slot = k // self.every - 1
@@ -515,6 +543,39 @@ class DeviceEngine:
                       self.history.data_ptr(), st)
         self._account(k, d, m, fresh, t)
 
+    def _candidate_split(self, WA, t, m):
+        """split(r) (partition.py:48-55), preconditioned as in solvers.py:331-336:
+        M^-1 split(r) when the factor blocks align with the subdomains, else
+        L^-T split(L^-1 r)."""
+        n, st, live = self.n, self.stream, self.live
+        owner = self.owner_dev.data_ptr()
+        pc = self.pc
+        if pc is None:
+            _lib.call("ekcg_split", self.r.data_ptr(), owner, WA, n, t, m, live, st)
+        elif self.pc_aligned:
+            _lib.call("ekcg_split", self.r.data_ptr(), owner, WA, n, t, m, live, st)
+            self._minv(WA, m, WA, m, t)
+        else:
+            pc.apply(pc.FORWARD, self.r.data_ptr(), 1, self.tmpv2.data_ptr(), 1, 1, live, st)
+            _lib.call("ekcg_split", self.tmpv2.data_ptr(), owner, WA, n, t, m, live, st)
+            pc.apply(pc.BACKWARD, WA, m, self.WC.data_ptr(), m, t, live, st)
+            _lib.call("ekcg_copy_cols", self.WC.data_ptr(), m, WA, m, n, t, live, st)
+
+    def _normed(self, v, live):
+        """Pointer to the vector whose 2-norm is the residual norm: v, or L v in explicit-hat mode."""
+        if self.norm_pc is None:
+            return v.data_ptr()
+        pc = self.norm_pc
+        pc.apply(pc.MULT_L, v.data_ptr(), 1, self.tmpv3.data_ptr(), 1, 1, live, self.stream)
+        return self.tmpv3.data_ptr()
+
+    def _minv(self, X, ldx, Y, ldy, w):
+        """Y = M^-1 X = L^-T L^-1 X (blockjacobi.py:155-157) through the scratch block WC."""
+        pc, st, live = self.pc, self.stream, self.live
+        scratch = self.WC.data_ptr() if w > 1 else self.tmpv3.data_ptr()
+        pc.apply(pc.FORWARD, X, ldx, scratch, w, w, live, st)
+        pc.apply(pc.BACKWARD, scratch, w, Y, ldy, w, live, st)
+
     def _chain(self, V, m, t):
         """s-step chain V^(i+1) = A V^(i) on column slabs of width t (s-step)."""
         for i in range(1, self.s):
@@ -525,7 +586,7 @@ class DeviceEngine:
         self._apply_op(x.data_ptr(), 1, self.tmpv.data_ptr(), 1, 1, tag="spmv", live=live)
         _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), self.tmpv.data_ptr(), self.n, live,
                   self.stream)
-        _lib.call("ekcg_sumsq", self.tmpv.data_ptr(), self.n, self.vpart.data_ptr(), live, self.stream)
+        _lib.call("ekcg_sumsq", self._normed(self.tmpv, live), self.n, self.vpart.data_ptr(), live, self.stream)
         _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, out.data_ptr(), live, self.stream)
 
     def _ensure_history(self, length):
@@ -545,9 +606,12 @@ class DeviceEngine:
         self.launch_k.append((k, d, m))
 
     def _nnz(self):
-        if hasattr(self.op, "nnz"):
-            return self.op.nnz
-        shape = self.op.shape
+        op = self.op
+        while getattr(op, "nnz", None) is None and hasattr(op, "op"):  # composite (explicit-hat) operator
+            op = op.op
+        if getattr(op, "nnz", None) is not None:
+            return op.nnz
+        shape = op.shape
         tot = self.n
         for ax in range(len(shape)):
             other = self.n // shape[ax]
@@ -662,7 +726,7 @@ class DeviceEngine:
         self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
         self._apply_op(self.x.data_ptr(), 1, self.tmpv.data_ptr(), 1, 1, tag="spmv", live=None)
         _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), self.r.data_ptr(), self.n, None, st)
-        _lib.call("ekcg_sumsq", self.r.data_ptr(), self.n, self.vpart.data_ptr(), None, st)
+        _lib.call("ekcg_sumsq", self._normed(self.r, None), self.n, self.vpart.data_ptr(), None, st)
         _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), None, st)
         self._allreduce(self.rho2)
         _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
@@ -705,7 +769,7 @@ class DeviceEngine:
         if status is None:
             # loop exhausted kmax without the device flag (cannot happen) or rho0 == 0
             status = "converged" if ctrl["last_rho"] <= ctrl["tol_abs"] else "maxiter"
-        notes = []
+        notes = list(self.notes_init)
         if status_code == 3:
             if ctrl["brk_kind"] == 1:
                 msg = f"zero column {ctrl['brk_col']} entering Pre-CholQR"

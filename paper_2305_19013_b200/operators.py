@@ -136,8 +136,37 @@ class StencilOperator:
 
 
 def as_operator(A, device=None):
-    if isinstance(A, (CsrOperator, StencilOperator)):
+    if isinstance(A, (CsrOperator, StencilOperator, HatOperator)):
         return A
     if hasattr(A, "row_ptr") and hasattr(A, "col_idx") and hasattr(A, "values"):
         return CsrOperator(A, device)
     raise TypeError(f"unsupported operator type {type(A).__name__}")
+
+
+class HatOperator:
+    """L^-1 A L^-T for the explicit-hat preconditioned mode (solvers.py:295-316)."""
+
+    kind = "hat"
+
+    def __init__(self, op, pc):
+        self.op, self.pc = op, pc
+        self.n = op.n
+        self.device = op.device
+        self.nnz = op.nnz if hasattr(op, "nnz") else None
+        self._tmp = {}
+
+    def matrix_bytes(self):
+        return self.op.matrix_bytes()
+
+    def _scratch(self, m):
+        if m not in self._tmp:
+            f64 = dict(dtype=torch.float64, device=self.device)
+            self._tmp[m] = (torch.empty(self.n * m, **f64), torch.empty(self.n * m, **f64))
+        return self._tmp[m]
+
+    def apply(self, X, ldx, Y, ldy, m, live=None, stream=None):
+        t1, t2 = self._scratch(m)
+        pc = self.pc
+        pc.apply(pc.BACKWARD, _ptr(X), ldx, t1.data_ptr(), m, m, live, stream)
+        self.op.apply(t1, m, t2, m, m, live, stream)
+        pc.apply(pc.FORWARD, t2.data_ptr(), m, _ptr(Y), ldy, m, live, stream)

@@ -34,6 +34,8 @@ class ShardedEngine(DeviceEngine):
     def __init__(self, op, partition, cfg, comm=None, device=None):
         if not isinstance(op, StencilOperator):
             raise TypeError("the sharded engine needs a StencilOperator")
+        if cfg.preconditioner is not None:
+            raise ValueError("the sharded engine runs unpreconditioned")
         if cfg.method not in ("sre-cg2", "sre-cg") or cfg.switch_tol is not None:
             raise ValueError("the sharded engine runs SRE-CG2 / SRE-CG without the flexible switch")
         super().__init__(op, partition, cfg, device=device)

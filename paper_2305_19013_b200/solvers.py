@@ -81,6 +81,8 @@ class SolverConfig:
             raise ValueError("s must be >= 1")
         if self.s > 1 and self.method not in ("sre-cg2", "sre-cg"):
             raise ValueError("the s-step variant is defined for sre-cg2 / sre-cg")
+        if self.s > 1 and self.preconditioner is not None:
+            raise ValueError("the s-step variant is not defined with preconditioning")
         if self.s * self.t > MAX_BLOCK_WIDTH:
             raise ValueError(f"block width s*t = {self.s * self.t} exceeds {MAX_BLOCK_WIDTH}")
         if self.true_residual_every < 1:
@@ -179,6 +181,38 @@ def _as_float_vec(v, n, name):
     return arr
 
 
+def _solve_explicit_hat(A, b, x0, partition, cfg, x_star, on_iteration, device):
+    """Plain engine on L^-1 A L^-T, x = L^-T x_hat (solvers.py:295-316), all on the device."""
+    from dataclasses import replace
+
+    import torch
+
+    from .device import as_device
+    from .engine import DeviceEngine
+    from .operators import HatOperator, as_operator
+    from .precond import DevicePreconditioner, backward_solve, forward_solve, mult_lt
+
+    op = as_operator(A, device)
+    F = cfg.preconditioner
+    pc = F if isinstance(F, DevicePreconditioner) else DevicePreconditioner(F, op.device)
+    b_hat = forward_solve(pc, b)
+    x0_hat = None if x0 is None else mult_lt(pc, x0)
+    engine = DeviceEngine(HatOperator(op, pc), partition, replace(cfg, preconditioner=None), device=device)
+    engine.norm_pc = pc
+    x_hat, rep = engine.solve(b_hat, x0_hat, on_iteration=on_iteration)
+    x = backward_solve(pc, x_hat)
+    xt, _ = as_device(x, device=op.device)
+    bt, _ = as_device(b, device=op.device)
+    ax = torch.empty_like(xt)
+    op.apply(xt, 1, ax, 1, 1)
+    rep.x = x
+    rep.true_residual = float(torch.linalg.vector_norm(bt - ax).item())
+    if x_star is not None:
+        xs, _ = as_device(x_star, device=op.device)
+        rep.relative_error = float((torch.linalg.vector_norm(xt - xs) / torch.linalg.vector_norm(xs)).item())
+    return x, rep
+
+
 def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iteration=None,
                    device=None):
     """Run one enlarged-CG method on the GPU (solvers.py:261-292).
@@ -205,8 +239,11 @@ def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iter
         raise ValueError(f"partition covers {partition.n} indices, matrix has {n}")
     b = _as_float_vec(b, n, "b")
     x0 = _as_float_vec(x0, n, "x0")
-    if cfg.preconditioner is not None:
-        raise NotImplementedError("split block-Jacobi preconditioning is not on the device path yet")
+    F = cfg.preconditioner
+    if F is not None and int(F.n) != n:
+        raise ValueError("preconditioner dimension does not match the matrix")
+    if F is not None and cfg.precond_mode == "explicit-hat":
+        return _solve_explicit_hat(A, b, x0, partition, cfg, x_star, on_iteration, device)
     import torch.distributed as tdist
     from .operators import StencilOperator
     sharded = (tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1
