@@ -30,6 +30,10 @@ long long rows_per_chunk(long long n, int chunks) {
 // Tuning knobs (ekcg_tune): m = 16 Gram variant and target CTA count.
 int g_gram16_variant = -1;   // -1: automatic by d (measured on B200, tools/tune_gram.py)
 long long g_gram_target = 0;  // 0: automatic
+}  // namespace
+int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
+int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
+namespace {
 constexpr int kGram16GB[] = {4, 2, 2, 4, 4, 4, 1};
 
 // Blocks per CTA that share one pass over Y (see gram_dmma_kernel).
@@ -531,6 +535,63 @@ xr_update_kernel(const double* __restrict__ W, int ldw, const double* __restrict
     if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
+// m = 4*LN columns, 16-B aligned rows: LN lanes per row, 4 columns per lane,
+// U row groups in flight per warp (x and r loaded before the reductions).
+template <int LN, int U>
+__global__ void __launch_bounds__(kVecThreads)
+xr_update4_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ AW, int ldaw,
+                  const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ r, long long n,
+                  double* __restrict__ partials, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    constexpr int RPW = 32 / LN;
+    const int lane = threadIdx.x & 31;
+    const int sub = lane / LN, li = lane % LN;
+    const double2 a01 = __ldg(reinterpret_cast<const double2*>(alpha) + 2 * li);
+    const double2 a23 = __ldg(reinterpret_cast<const double2*>(alpha) + 2 * li + 1);
+    const long long warp_global = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const long long warps_total = ((long long)gridDim.x * blockDim.x) >> 5;
+    double sq = 0.0;
+    for (long long base = warp_global * RPW * U; base < n; base += warps_total * RPW * U) {
+        double dx[U], dr[U], xv[U], rv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long row = base + u * RPW + sub;
+            dx[u] = dr[u] = xv[u] = rv[u] = 0.0;
+            if (row < n) {
+                const double2* w = reinterpret_cast<const double2*>(W + row * ldw) + 2 * li;
+                const double2* aw = reinterpret_cast<const double2*>(AW + row * ldaw) + 2 * li;
+                const double2 w0 = __ldg(w), w1 = __ldg(w + 1), v0 = __ldg(aw), v1 = __ldg(aw + 1);
+                if (li == 0) {
+                    xv[u] = x[row];
+                    rv[u] = r[row];
+                }
+                dx[u] = w0.x * a01.x + w0.y * a01.y + w1.x * a23.x + w1.y * a23.y;
+                dr[u] = v0.x * a01.x + v0.y * a01.y + v1.x * a23.x + v1.y * a23.y;
+            }
+        }
+#pragma unroll
+        for (int off = LN / 2; off > 0; off >>= 1) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                dx[u] += __shfl_xor_sync(0xffffffffu, dx[u], off);
+                dr[u] += __shfl_xor_sync(0xffffffffu, dr[u], off);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long row = base + u * RPW + sub;
+            if (row < n && li == 0) {
+                x[row] = xv[u] + dx[u];
+                const double rn = rv[u] - dr[u];
+                r[row] = rn;
+                sq += rn * rn;
+            }
+        }
+    }
+    double s = block_sum(sq);
+    if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
 __global__ void __launch_bounds__(kVecThreads)
 sumsq_kernel(const double* __restrict__ v, long long n, double* __restrict__ partials,
              const int* __restrict__ live) {
@@ -640,6 +701,14 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_gram_target = value;
         return EKCG_OK;
     }
+    if (key == 3 && value >= 0 && value <= 1) {
+        g_stencil_march = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 4 && value >= 0 && value <= 6) {
+        g_march_variant = (int)value;
+        return EKCG_OK;
+    }
     return EKCG_EINVAL;
 }
 
@@ -735,13 +804,21 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
     cudaStream_t st = as_stream(stream);
     const int g = vec_chunks(n);
 #define XR_LAUNCH(L) xr_update_kernel<L><<<g, kVecThreads, 0, st>>>(W, ldw, AW, ldaw, alpha, m, x, r, n, rho2_partials, live)
-    if (m >= 32) XR_LAUNCH(32);
+#define XR4_LAUNCH(LN) xr_update4_kernel<LN, 4><<<g, kVecThreads, 0, st>>>(W, ldw, AW, ldaw, alpha, x, r, n, rho2_partials, live)
+    const bool al = (ldw % 2 == 0) && (ldaw % 2 == 0) && ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(AW) |
+                                                           reinterpret_cast<uintptr_t>(alpha)) % 16 == 0);
+    if (al && m == 64) XR4_LAUNCH(16);
+    else if (al && m == 32) XR4_LAUNCH(8);
+    else if (al && m == 16) XR4_LAUNCH(4);
+    else if (al && m == 8) XR4_LAUNCH(2);
+    else if (m >= 32) XR_LAUNCH(32);
     else if (m >= 16) XR_LAUNCH(16);
     else if (m >= 8) XR_LAUNCH(8);
     else if (m >= 4) XR_LAUNCH(4);
     else if (m >= 2) XR_LAUNCH(2);
     else XR_LAUNCH(1);
 #undef XR_LAUNCH
+#undef XR4_LAUNCH
     ++g_ekcg_launches;
     return launch_status();
 }

@@ -241,6 +241,10 @@ extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int l
     const bool aligned = (ldx % 2 == 0) && (ldy % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
     n = s.row_end - s.row_begin;
+    if (g_stencil_march && launch_stencil_march(s, uf, X, ldx, Y, ldy, m, live, st) == EKCG_OK) {
+        ++g_ekcg_launches;
+        return launch_status();
+    }
     if (aligned && m % 4 == 0) {
         RowLaunch L = row_launch(n, m / 4);
         stencil_spmm_kernel<4><<<L.grid, L.block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, live);

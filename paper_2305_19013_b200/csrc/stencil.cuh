@@ -23,7 +23,64 @@ __device__ __forceinline__ double harmonic_face(double c, double klo, double khi
 struct UniformFaces {
     double fz, fy, fx;  // c * 2k^2/(2k)
     double bz, by, bx;  // c * k
+    double dint;        // diagonal of an interior node: ((((fz + fz) + fy) + fy) + fx) + fx
 };
+
+// Coefficients of the node (x, y, z): v[0..6] = z-, y-, x-, diag, x+, y+, z+
+// (absent neighbours: 0) and the presence mask (bit q = slot q present).
+__device__ __forceinline__ unsigned stencil_coef(const EkcgStencil& s, const UniformFaces& uf, unsigned x,
+                                                 unsigned y, unsigned z, double (&v)[7]) {
+    const unsigned nx = s.nx, ny = s.ny, nz = s.nz;
+    const bool three = (s.dim == 3);
+    double fzl = 0.0, fzh = 0.0, fyl = 0.0, fyh = 0.0, fxl = 0.0, fxh = 0.0;
+    double diag = 0.0;
+    if (s.kfield == nullptr) {
+        if (three) {
+            if (z < nz - 1) { fzh = uf.fz; diag = add_rn(diag, fzh); }
+            if (z > 0)      { fzl = uf.fz; diag = add_rn(diag, fzl); }
+            if (z == 0)      diag = add_rn(diag, uf.bz);
+            if (z == nz - 1) diag = add_rn(diag, uf.bz);
+        }
+        if (y < ny - 1) { fyh = uf.fy; diag = add_rn(diag, fyh); }
+        if (y > 0)      { fyl = uf.fy; diag = add_rn(diag, fyl); }
+        if (y == 0)      diag = add_rn(diag, uf.by);
+        if (y == ny - 1) diag = add_rn(diag, uf.by);
+        if (x < nx - 1) { fxh = uf.fx; diag = add_rn(diag, fxh); }
+        if (x > 0)      { fxl = uf.fx; diag = add_rn(diag, fxl); }
+        if (x == 0)      diag = add_rn(diag, uf.bx);
+        if (x == nx - 1) diag = add_rn(diag, uf.bx);
+    } else {
+        const unsigned txi = x / (unsigned)s.tx, tyi = y / (unsigned)s.ty, tzi = z / (unsigned)s.tz;
+        const unsigned rx = x - txi * s.tx, ry = y - tyi * s.ty, rz = z - tzi * s.tz;
+        const long long fx = s.fx, fxy = (long long)s.fx * s.fy;
+        const double* __restrict__ F = s.kfield;
+        const long long tc = tzi * fxy + tyi * fx + txi;
+        const double kc = __ldg(F + tc);
+        if (three) {
+            if (z < nz - 1) { fzh = harmonic_face(s.cz, kc, __ldg(F + tc + (rz + 1 == (unsigned)s.tz ? fxy : 0))); diag = add_rn(diag, fzh); }
+            if (z > 0)      { fzl = harmonic_face(s.cz, __ldg(F + tc - (rz == 0 ? fxy : 0)), kc); diag = add_rn(diag, fzl); }
+            if (z == 0)      diag = add_rn(diag, mul_rn(s.cz, kc));
+            if (z == nz - 1) diag = add_rn(diag, mul_rn(s.cz, kc));
+        }
+        if (y < ny - 1) { fyh = harmonic_face(s.cy, kc, __ldg(F + tc + (ry + 1 == (unsigned)s.ty ? fx : 0))); diag = add_rn(diag, fyh); }
+        if (y > 0)      { fyl = harmonic_face(s.cy, __ldg(F + tc - (ry == 0 ? fx : 0)), kc); diag = add_rn(diag, fyl); }
+        if (y == 0)      diag = add_rn(diag, mul_rn(s.cy, kc));
+        if (y == ny - 1) diag = add_rn(diag, mul_rn(s.cy, kc));
+        if (x < nx - 1) { fxh = harmonic_face(s.cx, kc, __ldg(F + tc + (rx + 1 == (unsigned)s.tx ? 1 : 0))); diag = add_rn(diag, fxh); }
+        if (x > 0)      { fxl = harmonic_face(s.cx, __ldg(F + tc - (rx == 0 ? 1 : 0)), kc); diag = add_rn(diag, fxl); }
+        if (x == 0)      diag = add_rn(diag, mul_rn(s.cx, kc));
+        if (x == nx - 1) diag = add_rn(diag, mul_rn(s.cx, kc));
+    }
+    v[0] = -fzl; v[1] = -fyl; v[2] = -fxl; v[3] = diag; v[4] = -fxh; v[5] = -fyh; v[6] = -fzh;
+    unsigned mk = 1u << 3;
+    if (three && z > 0)      mk |= 1u << 0;
+    if (y > 0)               mk |= 1u << 1;
+    if (x > 0)               mk |= 1u << 2;
+    if (x < nx - 1)          mk |= 1u << 4;
+    if (y < ny - 1)          mk |= 1u << 5;
+    if (three && z < nz - 1) mk |= 1u << 6;
+    return mk;
+}
 
 // Row i of the operator: neighbour offsets and values in column order.
 // Returns the entry count; `dpos` gets the position of the diagonal entry.
@@ -167,6 +224,22 @@ static inline int prepare_stencil(const EkcgStencil* desc, EkcgStencil& s, Unifo
         uf.bz = s.cz * s.kconst;
         uf.by = s.cy * s.kconst;
         uf.bx = s.cx * s.kconst;
+        volatile double d = 0.0;
+        if (s.dim == 3) {
+            d = d + uf.fz;
+            d = d + uf.fz;
+        }
+        d = d + uf.fy;
+        d = d + uf.fy;
+        d = d + uf.fx;
+        d = d + uf.fx;
+        uf.dint = d;
     }
     return EKCG_OK;
 }
+
+// Plane-marching stencil SpMM (stencil_march.cu); EKCG_EINVAL when it does not apply.
+int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy,
+                     int m, const int* live, cudaStream_t st);
+extern int g_stencil_march;  // ekcg_tune key 3
+extern int g_march_variant;  // ekcg_tune key 4

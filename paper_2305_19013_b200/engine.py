@@ -414,8 +414,9 @@ class DeviceEngine:
             _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, self._karg(k), 1e-14, st)
         self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WB, m, m, 0.0, 1.0, tag="tri_apply")
         finish_now = (k % self.every != 0)
-        if fused and "cholinv" in self.fuse:
-            # G = W0^T A W0 (A W0 never written) + A-CholQR factor S
+        if fused and "cholinv" in self.fuse and m <= 16:
+            # G = W0^T A W0 (A W0 never written) + A-CholQR factor S.  For m >= 32
+            # the unfused stencil + DMMA Gram is faster (kernel_times.py --fused).
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WB, m, m, part.data_ptr(), self.counter.data_ptr(),
                 self.S.data_ptr(), live, self._karg(k), 1e-14, 1, st))
@@ -432,7 +433,8 @@ class DeviceEngine:
             self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
                          tag="tri_apply")
             self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
-        xr_fused = fused and "xr" in self.fuse
+        # m >= 32: the plane-marching stencil + xr_update beats the fused row kernel
+        xr_fused = fused and "xr" in self.fuse and m <= 16
         if xr_fused:
             # AW_k = A W_k + x/r update + |r|^2 + end-of-iteration bookkeeping (solvers.py:394-415)
             self._ensure_history(k + 1)
@@ -503,22 +505,25 @@ class DeviceEngine:
         self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
         _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, self._karg(k), 1e-14, st)
         self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WC, m, m, 0.0, 1.0, tag="tri_apply")  # W0 -> WC
-        if fused:
+        if fused and m <= 16:
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WC, m, m, part.data_ptr(), self.counter.data_ptr(),
                 self.S.data_ptr(), live, self._karg(k), 1e-14, 1, st))
-            self._timed("tri_alpha", lambda: _lib.call(
-                "ekcg_update_vec", WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
-                part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
         else:
             self._apply_op(WC, m, WA, m, m)  # A W0 -> WA (free)
             self._gram(WC_arr, m, 1, m, WA, m, m, self.G.data_ptr(), tag="gram_self")
             _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, self._karg(k), 1e-14, st)
+        if fused:
+            self._timed("tri_alpha", lambda: _lib.call(
+                "ekcg_update_vec", WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
+                part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
+        else:
             self._update(WC_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
                          tag="tri_apply")
             self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
         finish_now = (k % self.every != 0)
-        if fused:
+        xr_fused = fused and m <= 16
+        if xr_fused:
             self._ensure_history(k + 1)
             self._timed("spmm_xr", lambda: _lib.call(
                 "ekcg_stencil_xr", self.op.desc_ref(), blk.q.data_ptr(), m, WA, m, m,
@@ -537,7 +542,7 @@ class DeviceEngine:
             self._ensure_checks(slot + 1)
             self._residual_sq(self.x, self.tr2, live)
             _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
-        if not (fused and finish_now):
+        if not (xr_fused and finish_now):
             self._ensure_history(k + 1)
             _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), self._karg(k), self.kmax, self.stag_window,
                       self.history.data_ptr(), st)

@@ -197,8 +197,11 @@ class ShardedEngine(DeviceEngine):
         self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, lWB, m, m, 0.0, 1.0, tag="tri_apply")
         self.comm.halo_exchange(self.WB, m, self.shard)
         fused = m in (8, 16, 32, 64)
+        # same kernel choice as DeviceEngine: the fused stencil kernels only for
+        # m <= 16, the plane-marching stencil + DMMA kernels above
+        fused_st = fused and m <= 16
         part = self._ensure("part", max(self.fused_part, 1)) if fused else None
-        if fused:
+        if fused_st:
             _lib.call("ekcg_stencil_cholinv", ctypes.byref(self._desc), self._gptr_ext(self.WB, m), m, m,
                       part.data_ptr(), self.counter.data_ptr(), self.G.data_ptr(), live, k, 1e-14, 0, st)
         else:
@@ -216,7 +219,7 @@ class ShardedEngine(DeviceEngine):
 
         # ---- AW_k = A W_k and the iterate update ----
         self.comm.halo_exchange(blk.q, m, self.shard)
-        if fused:
+        if fused_st:
             _lib.call("ekcg_stencil_xr", ctypes.byref(self._desc), self._gptr_ext(blk.q, m), m,
                       self._gptr_loc(blk.aq, m), m, m, self.alpha.data_ptr(), self._gptr_ext(self.x, 1),
                       self._gptr_loc(self.r, 1), part.data_ptr(), self.counter.data_ptr(), live, k, self.kmax,

@@ -71,6 +71,54 @@ def test_stencil_equals_csr_bitwise(idx, edge, m):
     assert np.array_equal(pk.spmm(A, X), ref)
 
 
+@pytest.mark.parametrize("shape,kappa", [((17, 5, 9), None), ((67, 3), None), ((33, 33, 3), "tile"),
+                                         ((2, 2, 2), None), ((130, 7), "node"), ((21, 19, 11), "node")])
+@pytest.mark.parametrize("m", [4, 12, 16, 20, 64])
+def test_stencil_march_kernel(shape, kappa, m):
+    """Plane-marching kernel (ekcg_tune key 3) vs the row kernel vs the CSR oracle,
+    on ragged tiles, partial column chunks and plane-aligned row ranges."""
+    import ctypes
+    rng = np.random.default_rng(len(shape) * 1000 + m + shape[0])
+    n = int(np.prod(shape))
+    if kappa == "tile":
+        tile = (4,) * len(shape)
+        need = tuple(-(-s // 4) for s in shape)[::-1]
+        op = pk.StencilOperator(shape, 10.0 ** rng.uniform(-2, 2, need), tile=tile)
+    elif kappa == "node":
+        op = pk.StencilOperator(shape, 10.0 ** rng.uniform(-3, 3, n))
+    else:
+        op = pk.StencilOperator(shape, 2.5)
+    A = op.to_csr()
+    X = rng.standard_normal((n, m))
+    X[::3, 1] = 0.0
+    ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, X)
+    Xd = dev(X)
+    outs = []
+    try:
+        for march in (1, 0):
+            assert _lib.query("ekcg_tune", 3, march) == 0
+            Yd = torch.full_like(Xd, np.nan)
+            op.apply(Xd, m, Yd, m, m)
+            outs.append(Yd.cpu().numpy())
+        # plane-aligned row range (one shard's slab), march on
+        assert _lib.query("ekcg_tune", 3, 1) == 0
+        plane = n // shape[-1]
+        lo, hi = plane * (shape[-1] // 3), plane * max(shape[-1] // 3 + 1, (2 * shape[-1]) // 3)
+        d = op._desc
+        sub = type(d)()
+        ctypes.pointer(sub)[0] = d
+        sub.row_begin, sub.row_end = lo, hi
+        Yd = torch.full_like(Xd, np.nan)
+        _lib.call("ekcg_spmm_stencil", ctypes.byref(sub), Xd.data_ptr(), m, Yd.data_ptr(), m, m, None, stream())
+        part = Yd.cpu().numpy()
+    finally:
+        _lib.query("ekcg_tune", 3, 1)
+    assert np.array_equal(outs[0], ref)
+    assert np.array_equal(outs[1], ref)
+    assert np.array_equal(part[lo:hi], ref[lo:hi])
+    assert np.isnan(part[:lo]).all() and np.isnan(part[hi:]).all()
+
+
 def test_spmm_strided_slabs():
     prob = make_config(2, 8)
     op = prob.stencil()

@@ -1,0 +1,5 @@
+# plane-marching stencil: parity + A/B timings
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "stencil" 2>&1 | tail -5
+timeout 300 python tools/kernel_times.py --stencil 2>&1 | tail -12
+timeout 600 python tools/breakdown.py --config 3 --kmax 300 2>&1 | tail -1

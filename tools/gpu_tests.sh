@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout 1500 python -m pytest tests -q -m gpu -x 2>&1 | tail -4
+timeout 600 python tools/breakdown.py --config 3 --kmax 300 2>&1 | tail -1
+timeout 1200 python tools/run_configs.py --configs 3,4 2>&1 | cut -c1-300

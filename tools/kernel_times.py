@@ -58,7 +58,7 @@ def sweep(m, shape, d):
     return out
 
 
-if __name__ == "__main__" and "--fused" not in sys.argv:
+if __name__ == "__main__" and "--fused" not in sys.argv and "--stencil" not in sys.argv:
     cases = [(16, (64, 64, 64), 32), (16, (64, 64, 64), 110), (32, (128, 128, 128), 4), (64, (256, 256, 128), 3),
              (64, (256, 256, 256), 2)]
     res = {}
@@ -105,3 +105,32 @@ def fused_times():
 
 if __name__ == "__main__" and "--fused" in sys.argv:
     fused_times()
+
+
+def stencil_ab():
+    """Plane-marching vs row-parallel stencil kernel (ekcg_tune 3) at config sizes."""
+    import numpy as np
+    cases = [(16, (64, 64, 64), None), (16, (128, 128, 128), None), (32, (128, 128, 128), None),
+             (64, (256, 256, 128), None), (16, (128, 128, 128), "node"), (32, (2048, 2048), None),
+             (8, (128, 128, 128), None), (4, (256, 256, 256), None)]
+    for m, shape, kap in cases:
+        n = int(np.prod(shape))
+        kappa = 1.0 if kap is None else np.exp(np.random.default_rng(0).standard_normal(n))
+        op = StencilOperator(shape, kappa)
+        X = torch.randn(n * m, dtype=torch.float64, device=dev)
+        Y = torch.empty_like(X)
+        row = {}
+        for march in (0, 1):
+            _lib.call("ekcg_tune", 3, march)
+            for var in ((0, 2, 4, 5, 6) if march and len(shape) == 3 and m % 16 == 0 else (0,)):
+                _lib.call("ekcg_tune", 4, var)
+                t = timeit(lambda: op.apply(X, m, Y, m, m), reps=10)
+                row[f"march{var}" if march else "row"] = round((16 * n * m + op.matrix_bytes()) / t / 1e9)
+        _lib.call("ekcg_tune", 4, 0)
+        print(f"m{m} {'x'.join(map(str, shape))} {kap or 'const'}", row, flush=True)
+        del X, Y, op
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__" and "--stencil" in sys.argv:
+    stencil_ab()
