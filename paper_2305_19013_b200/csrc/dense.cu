@@ -31,8 +31,18 @@ long long rows_per_chunk(long long n, int chunks) {
 int g_gram16_variant = -1;   // -1: automatic by d (measured on B200, tools/tune_gram.py)
 long long g_gram_target = 0;  // 0: automatic
 }  // namespace
+int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
+                       int chunks, long long rows_chunk, double* partials, const int* live, cudaStream_t st);
+extern int g_gram_stream;
+int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
+                         double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
+                         cudaStream_t st);
+extern int g_update_stream;
+
 int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
+int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
+int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
 namespace {
 constexpr int kGram16GB[] = {4, 2, 2, 4, 4, 4, 1};
 
@@ -51,13 +61,41 @@ int gram_blocks_per_cta(int d, int m1, int m2) {
 }
 
 // ---------------------------------------------------------------------------
+// Fragment loads with column interleave.  A DMMA m8n8k4 operand lane (i, k)
+// holds element i of an 8-wide tile; with T >= 2 tiles the tiles are
+// interleaved over the row segment -- tile t, element i is column
+// (t / 2) * 16 + 2 i + (t % 2) -- so one 16-B load per lane feeds two tiles and
+// a warp load covers whole 128-B row segments.  Odd T: plain 8-column tiles.
+// (16-B aligned rows required: even leading dimensions, aligned blocks.)
+// ---------------------------------------------------------------------------
+template <int T, bool IL = true>
+__device__ __forceinline__ int tile_col(int t, int i) {
+    return (IL && T % 2 == 0) ? (t / 2) * 16 + 2 * i + (t % 2) : 8 * t + i;
+}
+
+template <int T, bool IL = true>
+__device__ __forceinline__ void load_tiles(const double* row, int lc, bool ok, double (&f)[T]) {
+    if (IL && T % 2 == 0) {
+#pragma unroll
+        for (int h = 0; h < T / 2; ++h) {
+            const double2 v = ok ? __ldg(reinterpret_cast<const double2*>(row + 16 * h + 2 * lc)) : make_double2(0.0, 0.0);
+            f[2 * h] = v.x;
+            f[2 * h + 1] = v.y;
+        }
+    } else {
+#pragma unroll
+        for (int t = 0; t < T; ++t) f[t] = ok ? __ldg(row + 8 * t + lc) : 0.0;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // DMMA Gram: partials[p][i] (M x M) = X_i[rows of p]^T Y[rows of p]
 // CTA (p, g) handles row chunk p for blocks i = g*GB .. g*GB+GB-1, so each Y
 // fragment loaded feeds GB blocks.  Warp w: row lane ks = w % KS, output
 // quadrant q = w / KS with TA x TB tiles of 8x8.  Rows advance in k-steps of
 // 4 (the mma K); fragments come straight from the row-major blocks.
 // ---------------------------------------------------------------------------
-template <int M, int TA, int TB, int KS, int U, int GB>
+template <int M, int TA, int TB, int KS, int U, int GB, bool IL>
 __global__ void __launch_bounds__(kGramThreads)
 gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const double* __restrict__ Y, int ldy,
                  long long n, long long rows_chunk, double* __restrict__ partials,
@@ -100,16 +138,9 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
             long long s = s0 + (long long)u * KS;
             long long r = r0 + 4 * s + lr;
             bool ok = (s < steps) && (r < r1);
-            const double* yrow = Y + r * ldy + b_base + lc;
+            load_tiles<TB, IL>(Y + r * ldy + b_base, lc, ok, bf[u]);
 #pragma unroll
-            for (int tb = 0; tb < TB; ++tb) bf[u][tb] = ok ? __ldg(yrow + 8 * tb) : 0.0;
-#pragma unroll
-            for (int g = 0; g < GB; ++g) {
-                const double* xrow = X[g] + r * ldx + a_base + lc;
-                bool okg = ok && (g < nb);
-#pragma unroll
-                for (int ta = 0; ta < TA; ++ta) af[u][g][ta] = okg ? __ldg(xrow + 8 * ta) : 0.0;
-            }
+            for (int g = 0; g < GB; ++g) load_tiles<TA, IL>(X[g] + r * ldx + a_base, lc, ok && (g < nb), af[u][g]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -130,10 +161,9 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
             for (int ta = 0; ta < TA; ++ta)
 #pragma unroll
                 for (int tb = 0; tb < TB; ++tb) {
-                    int a = a_base + 8 * ta + lc;
-                    int b = b_base + 8 * tb + 2 * lr;
-                    out[a * M + b] = acc[g][ta][tb][0];
-                    out[a * M + b + 1] = acc[g][ta][tb][1];
+                    const int a = a_base + tile_col<TA, IL>(ta, lc);
+                    out[a * M + b_base + tile_col<TB, IL>(tb, 2 * lr)] = acc[g][ta][tb][0];
+                    out[a * M + b_base + tile_col<TB, IL>(tb, 2 * lr + 1)] = acc[g][ta][tb][1];
                 }
         }
     } else {
@@ -143,10 +173,9 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
             for (int ta = 0; ta < TA; ++ta)
 #pragma unroll
                 for (int tb = 0; tb < TB; ++tb) {
-                    int a = a_base + 8 * ta + lc;
-                    int b = b_base + 8 * tb + 2 * lr;
-                    red[((ks * GB + g) * M + a) * M + b] = acc[g][ta][tb][0];
-                    red[((ks * GB + g) * M + a) * M + b + 1] = acc[g][ta][tb][1];
+                    const int a = a_base + tile_col<TA, IL>(ta, lc);
+                    red[((ks * GB + g) * M + a) * M + b_base + tile_col<TB, IL>(tb, 2 * lr)] = acc[g][ta][tb][0];
+                    red[((ks * GB + g) * M + a) * M + b_base + tile_col<TB, IL>(tb, 2 * lr + 1)] = acc[g][ta][tb][1];
                 }
         __syncthreads();
         for (int o = threadIdx.x; o < nb * M * M; o += kGramThreads) {
@@ -165,28 +194,31 @@ using GramFn = void (*)(const double* const*, int, int, const double*, int, long
 // The DMMA Gram variant for (d, m1, m2) (nullptr: generic kernel) and its GB.
 GramFn select_gram(int d, int m1, int m2, int& gb) {
     gb = gram_blocks_per_cta(d, m1, m2);
+    // interleaved loads: faster for m = 32 and for m = 16 with short histories,
+    // slower for m = 16 with d >= 48 and for m = 64 (tools/kernel_times.py)
+    const bool il = g_frag_il >= 0 ? g_frag_il == 1 : (m1 == 32 || (m1 == 16 && d < 48));
     if (m1 != m2) return nullptr;
     switch (m1) {
         case 8:
-            if (gb == 8) return gram_dmma_kernel<8, 1, 1, 4, 4, 8>;
-            if (gb == 4) return gram_dmma_kernel<8, 1, 1, 4, 4, 4>;
-            if (gb == 2) return gram_dmma_kernel<8, 1, 1, 4, 4, 2>;
-            return gram_dmma_kernel<8, 1, 1, 4, 4, 1>;
+            if (gb == 8) return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 8, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 8, false>;
+            if (gb == 4) return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 4, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 4, false>;
+            if (gb == 2) return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 2, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 2, false>;
+            return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 1, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 1, false>;
         case 16: {
             const int v = g_gram16_variant >= 0 ? g_gram16_variant : (d >= 48 ? 0 : 3);
-            if (gb == 1) return gram_dmma_kernel<16, 2, 2, 4, 4, 1>;
-            if ((v == 1 || g_gram16_variant < 0) && gb == 2) return gram_dmma_kernel<16, 2, 2, 4, 4, 2>;
-            if (gb == 2) return gram_dmma_kernel<16, 2, 2, 4, 2, 2>;
-            if (v == 3 && gb == 4) return gram_dmma_kernel<16, 2, 2, 4, 1, 4>;
-            if (v == 5 && gb == 4) return gram_dmma_kernel<16, 2, 1, 2, 4, 4>;
-            if (v == 4 && gb == 4) return gram_dmma_kernel<16, 2, 2, 4, 4, 4>;
-            return gram_dmma_kernel<16, 2, 2, 4, 2, 4>;
+            if (gb == 1) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 1, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 1, false>;
+            if ((v == 1 || g_gram16_variant < 0) && gb == 2) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 2, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 2, false>;
+            if (gb == 2) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 2, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 2, false>;
+            if (v == 3 && gb == 4) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 1, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 1, 4, false>;
+            if (v == 5 && gb == 4) return il ? (GramFn)gram_dmma_kernel<16, 2, 1, 2, 4, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 1, 2, 4, 4, false>;
+            if (v == 4 && gb == 4) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 4, false>;
+            return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 4, false>;
         }
         case 32:
-            if (gb == 2) return gram_dmma_kernel<32, 4, 2, 2, 2, 2>;
-            return gram_dmma_kernel<32, 4, 2, 2, 4, 1>;
+            if (gb == 2) return il ? (GramFn)gram_dmma_kernel<32, 4, 2, 2, 2, 2, true> : (GramFn)gram_dmma_kernel<32, 4, 2, 2, 2, 2, false>;
+            return il ? (GramFn)gram_dmma_kernel<32, 4, 2, 2, 4, 1, true> : (GramFn)gram_dmma_kernel<32, 4, 2, 2, 4, 1, false>;
         case 64:
-            return gram_dmma_kernel<64, 4, 4, 1, 2, 1>;
+            return il ? (GramFn)gram_dmma_kernel<64, 4, 4, 1, 2, 1, true> : (GramFn)gram_dmma_kernel<64, 4, 4, 1, 2, 1, false>;
         default:
             return nullptr;
     }
@@ -310,7 +342,31 @@ reduce_kernel(const double* __restrict__ partials, int chunks, long long len, do
 // Warp tile: 8*MR rows x M columns; mma M-dim = rows, N = output column,
 // K = column of Q_i.
 // ---------------------------------------------------------------------------
-template <int M, int MR>
+// Wout[r, b:b+2] = beta Win[r, b:b+2] + sign acc for the accumulator pairs of
+// MR 8-row tiles (16-B loads / stores: even leading dimensions, aligned rows).
+template <int MR, int NT>
+__device__ __forceinline__ void store_tile_rows(const double (&acc)[MR][NT][2], long long rbase, int lc, int lr,
+                                                long long n, const double* Win, int ldwi, double* Wout, int ldwo,
+                                                double beta, double sign) {
+#pragma unroll
+    for (int mr = 0; mr < MR; ++mr) {
+        const long long r = rbase + 8 * mr + lc;
+        if (r >= n) continue;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+            const int b = 8 * nt + 2 * lr;
+            double2 o = make_double2(sign * acc[mr][nt][0], sign * acc[mr][nt][1]);
+            if (beta != 0.0) {
+                const double2 wi = *reinterpret_cast<const double2*>(Win + r * ldwi + b);
+                o.x = beta * wi.x + o.x;
+                o.y = beta * wi.y + o.y;
+            }
+            *reinterpret_cast<double2*>(Wout + r * ldwo + b) = o;
+        }
+    }
+}
+
+template <int M, int MR, bool IL = true>
 __global__ void __launch_bounds__(128)
 update_dmma_kernel(const double* const* __restrict__ Qs, int ldq, int d, const double* __restrict__ C,
                    const double* Win, int ldwi, double* Wout, int ldwo, double beta, double sign,
@@ -335,40 +391,52 @@ update_dmma_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
         for (int i = 0; i < d; ++i) {
             const double* __restrict__ Q = Qs[i];
             const double* __restrict__ Ci = C + (long long)i * M * M;
+            if (!IL) {
 #pragma unroll
-            for (int kk = 0; kk < KK; ++kk) {
-                double bfr[NT];
+                for (int kk = 0; kk < KK; ++kk) {
+                    double bfr[NT];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) bfr[nt] = __ldg(Ci + (4 * kk + lr) * M + 8 * nt + lc);
-                double afr[MR];
+                    for (int nt = 0; nt < NT; ++nt) bfr[nt] = __ldg(Ci + (4 * kk + lr) * M + 8 * nt + lc);
+                    double afr[MR];
+#pragma unroll
+                    for (int mr = 0; mr < MR; ++mr) {
+                        long long r = rbase + 8 * mr + lc;
+                        afr[mr] = (r < n) ? __ldg(Q + r * ldq + 4 * kk + lr) : 0.0;
+                    }
+#pragma unroll
+                    for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+                        for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr], bfr[nt]);
+                }
+                continue;
+            }
+#pragma unroll
+            for (int kp = 0; kp < KK / 2; ++kp) {
+                // two k-steps per 16-B load: k index lr <-> columns 8 kp + 2 lr (+1)
+                double2 afr[MR];
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr) {
                     long long r = rbase + 8 * mr + lc;
-                    afr[mr] = (r < n) ? __ldg(Q + r * ldq + 4 * kk + lr) : 0.0;
+                    afr[mr] = (r < n) ? __ldg(reinterpret_cast<const double2*>(Q + r * ldq + 8 * kp + 2 * lr))
+                                      : make_double2(0.0, 0.0);
+                }
+                double bx[NT], by[NT];
+#pragma unroll
+                for (int nt = 0; nt < NT; ++nt) {
+                    bx[nt] = __ldg(Ci + (8 * kp + 2 * lr) * M + 8 * nt + lc);
+                    by[nt] = __ldg(Ci + (8 * kp + 2 * lr + 1) * M + 8 * nt + lc);
                 }
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr], bfr[nt]);
+                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr].x, bx[nt]);
+#pragma unroll
+                for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr].y, by[nt]);
             }
         }
-#pragma unroll
-        for (int mr = 0; mr < MR; ++mr) {
-            long long r = rbase + 8 * mr + lc;
-            if (r >= n) continue;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                int b = 8 * nt + 2 * lr;
-                double o0 = sign * acc[mr][nt][0];
-                double o1 = sign * acc[mr][nt][1];
-                if (beta != 0.0) {
-                    o0 = beta * Win[r * ldwi + b] + o0;
-                    o1 = beta * Win[r * ldwi + b + 1] + o1;
-                }
-                Wout[r * ldwo + b] = o0;
-                Wout[r * ldwo + b + 1] = o1;
-            }
-        }
+        store_tile_rows<MR, NT>(acc, rbase, lc, lr, n, Win, ldwi, Wout, ldwo, beta, sign);
     }
 }
 
@@ -407,40 +475,32 @@ update_smem_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
         for (int i = 0; i < d; ++i) {
             const double* __restrict__ Q = Qs[i];
             const double* Ci = cs + i * M * LDC;
-#pragma unroll 4
-            for (int kk = 0; kk < KK; ++kk) {
-                double afr[MR];
+#pragma unroll 2
+            for (int kp = 0; kp < KK / 2; ++kp) {
+                double2 afr[MR];
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr) {
                     long long r = rbase + 8 * mr + lc;
-                    afr[mr] = (r < n) ? __ldg(Q + r * ldq + 4 * kk + lr) : 0.0;
+                    afr[mr] = (r < n) ? __ldg(reinterpret_cast<const double2*>(Q + r * ldq + 8 * kp + 2 * lr))
+                                      : make_double2(0.0, 0.0);
                 }
-                double bfr[NT];
+                double bx[NT], by[NT];
 #pragma unroll
-                for (int nt = 0; nt < NT; ++nt) bfr[nt] = Ci[(4 * kk + lr) * LDC + 8 * nt + lc];
+                for (int nt = 0; nt < NT; ++nt) {
+                    bx[nt] = Ci[(8 * kp + 2 * lr) * LDC + 8 * nt + lc];
+                    by[nt] = Ci[(8 * kp + 2 * lr + 1) * LDC + 8 * nt + lc];
+                }
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr], bfr[nt]);
+                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr].x, bx[nt]);
+#pragma unroll
+                for (int mr = 0; mr < MR; ++mr)
+#pragma unroll
+                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr].y, by[nt]);
             }
         }
-#pragma unroll
-        for (int mr = 0; mr < MR; ++mr) {
-            long long r = rbase + 8 * mr + lc;
-            if (r >= n) continue;
-#pragma unroll
-            for (int nt = 0; nt < NT; ++nt) {
-                int b = 8 * nt + 2 * lr;
-                double o0 = sign * acc[mr][nt][0];
-                double o1 = sign * acc[mr][nt][1];
-                if (beta != 0.0) {
-                    o0 = beta * Win[r * ldwi + b] + o0;
-                    o1 = beta * Win[r * ldwi + b + 1] + o1;
-                }
-                Wout[r * ldwo + b] = o0;
-                Wout[r * ldwo + b + 1] = o1;
-            }
-        }
+        store_tile_rows<MR, NT>(acc, rbase, lc, lr, n, Win, ldwi, Wout, ldwo, beta, sign);
     }
 }
 
@@ -705,6 +765,22 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_stencil_march = (int)value;
         return EKCG_OK;
     }
+    if (key == 8 && value >= 0 && value <= 7) {
+        g_update_stream = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 7 && value >= 0 && value <= 8) {
+        g_gram_stream = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 6 && value >= 0 && value <= 1) {
+        g_upd_il = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 5 && value >= -1 && value <= 1) {
+        g_frag_il = (int)value;
+        return EKCG_OK;
+    }
     if (key == 4 && value >= 0 && value <= 6) {
         g_march_variant = (int)value;
         return EKCG_OK;
@@ -727,7 +803,12 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     cudaStream_t st = as_stream(stream);
     int gbs;
     GramFn fn = select_gram(d, m1, m2, gbs);
-    if (fn != nullptr) {
+    // DMMA variants with m >= 16 load 16-B fragments pairs: even leading
+    // dimensions, 16-B aligned Y (and blocks, by contract); else generic.
+    if (m1 >= 16 && ((ldx | ldy) % 2 != 0 || (reinterpret_cast<uintptr_t>(Y) & 15))) fn = nullptr;
+    if (fn != nullptr && launch_gram_stream(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, partials, live, st) == EKCG_OK) {
+        // streamed (TMA bulk) Gram, stream.cu
+    } else if (fn != nullptr) {
         fn<<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else {
         const int O = m1 * m2;
@@ -756,16 +837,20 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
     if (beta != 0.0 && (Win == nullptr || ldwi < m2)) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
     cudaStream_t st = as_stream(stream);
-    const bool even = (ldwo % 2 == 0) && (beta == 0.0 || ldwi % 2 == 0);
+    // DMMA kernels move 16-B pairs: even leading dimensions, aligned rows
+    const bool even = (ldwo % 2 == 0) && (ldq % 2 == 0) && (beta == 0.0 || ldwi % 2 == 0) &&
+                      ((reinterpret_cast<uintptr_t>(Wout) | reinterpret_cast<uintptr_t>(beta != 0.0 ? Win : Wout)) % 16 == 0);
     auto grid_rows = [&](int rows_per_warp) {
         long long tiles = (n + rows_per_warp - 1) / rows_per_warp;
         return grid_for(tiles, 4, 148LL * 16);
     };
-    if (m1 == m2 && even && m1 == 8) {
-        update_dmma_kernel<8, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+    if (launch_update_stream(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo, m2, beta, sign, n, live, st) == EKCG_OK) {
+        // streamed (TMA bulk) update, stream.cu
+    } else if (m1 == m2 && even && m1 == 8) {
+        (g_upd_il ? update_dmma_kernel<8, 4, true> : update_dmma_kernel<8, 4, false>)<<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                   sign, n, live);
     } else if (m1 == m2 && even && m1 == 16) {
-        update_dmma_kernel<16, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        (g_upd_il ? update_dmma_kernel<16, 4, true> : update_dmma_kernel<16, 4, false>)<<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
     } else if (m1 == m2 && even && (m1 == 32 || m1 == 64) && (size_t)d * m1 * (m1 + 4) * 8 <= 200 * 1024) {
         const size_t smem = (size_t)d * m1 * (m1 + 4) * sizeof(double);

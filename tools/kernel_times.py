@@ -39,14 +39,25 @@ def sweep(m, shape, d):
     W = torch.randn(n * m, dtype=torch.float64, device=dev)
     tab = torch.tensor([x.data_ptr() for x in Xs], dtype=torch.int64, device=dev)
     chunks = _lib.query("ekcg_gram_chunks", n, d, m, m)
-    part = torch.empty(max(chunks * d * m * m, 1 << 20), dtype=torch.float64, device=dev)
+    part = torch.empty(max(2048 * d * m * m, 1 << 20), dtype=torch.float64, device=dev)
     C = torch.randn(d * m * m, dtype=torch.float64, device=dev) * 0.01
-    g = timeit(lambda: _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Y.data_ptr(), m, m, n, part.data_ptr(),
-                                 None, st))
-    out["gram"] = dict(s=g, GBs=8 * (d + 1) * n * m / g / 1e9, TF=2 * d * m * m * n / g / 1e12)
-    u = timeit(lambda: _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m,
-                                 W.data_ptr(), m, m, 1.0, -1.0, n, None, st))
-    out["update"] = dict(s=u, GBs=8 * (d + 2) * n * m / u / 1e9, TF=2 * d * m * m * n / u / 1e12)
+    for gs in ((0, 3) if m == 16 else (0,)):
+        for tgt in (0,):
+            _lib.call("ekcg_tune", 7, gs)
+            _lib.call("ekcg_tune", 2, tgt)
+            ch = _lib.query("ekcg_gram_chunks", n, d, m, m)
+            g = timeit(lambda: _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Y.data_ptr(), m, m, n, part.data_ptr(),
+                                         None, st))
+            out[f"gram_s{gs}_t{tgt}"] = dict(s=g, GBs=8 * (d + 1) * n * m / g / 1e9, TF=2 * d * m * m * n / g / 1e12)
+    _lib.call("ekcg_tune", 7, 3)
+    _lib.call("ekcg_tune", 2, 0)
+    _lib.call("ekcg_tune", 5, -1)
+    for us in ((0, 2, 5, 6, 7) if m == 16 else (0,)):
+        _lib.call("ekcg_tune", 8, us)
+        u = timeit(lambda: _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m,
+                                     W.data_ptr(), m, m, 1.0, -1.0, n, None, st))
+        out[f"update_s{us}"] = dict(s=u, GBs=8 * (d + 2) * n * m / u / 1e9, TF=2 * d * m * m * n / u / 1e12)
+    _lib.call("ekcg_tune", 8, 2)
     op = StencilOperator(shape, 1.0)
     Z = torch.empty_like(Y)
     sp = timeit(lambda: op.apply(Y, m, Z, m, m))
