@@ -38,6 +38,7 @@ int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const 
                          double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                          cudaStream_t st);
 extern int g_update_stream;
+extern int g_march_fused;
 
 int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
@@ -250,6 +251,13 @@ int gram_chunks(long long n, int d, int m1, int m2) {
     int gb;
     GramFn fn = select_gram(d, m1, m2, gb);
     const long long groups = (d + gb - 1) / gb;
+    if (m1 == 16 && m2 == 16 && g_gram_stream && g_gram_target <= 0) {
+        // streamed Gram: one CTA per SM with long row ranges, one wave
+        long long p = (groups >= 148) ? 1 : 148 / groups;
+        const long long max_p = (n + 255) / 256;
+        if (p > max_p) p = max_p;
+        return (int)(p < 1 ? 1 : p);
+    }
     long long target = g_gram_target;
     if (target <= 0) {
         const long long waves = (m1 == 16 && m2 == 16 && d >= 48) ? 2 : 1;
@@ -763,6 +771,10 @@ extern "C" int ekcg_tune(int key, long long value) {
     }
     if (key == 3 && value >= 0 && value <= 1) {
         g_stencil_march = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 9 && value >= 0 && value <= 1) {
+        g_march_fused = (int)value;
         return EKCG_OK;
     }
     if (key == 8 && value >= 0 && value <= 7) {

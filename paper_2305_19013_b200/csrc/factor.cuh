@@ -76,6 +76,80 @@ __device__ inline void tri_inverse(const double* R, double* S, int m) {
     __syncthreads();
 }
 
+// Fixed-width fast path (M = 8, 16, 32): right-looking Cholesky with a
+// CTA-parallel trailing update (two barriers per column), then S = R^-1 with
+// one thread per column, the column kept in registers (fully unrolled).  A is
+// the symmetric input (smem, overwritten); R and S (smem) get the factor and
+// its inverse.  Same breakdown test as chol_rows.  Returns -1 or the column.
+template <int M>
+__device__ inline int chol_inv_fixed(double* A, double* R, double* S, double tol, double& piv_out,
+                                     double& scale_out) {
+    __shared__ double s_rinv[M];
+    __shared__ double s_scale;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nthr = blockDim.x * blockDim.y;
+    for (int e = tid; e < M * M; e += nthr) R[e] = 0.0;
+    if (tid == 0) {
+        double sc = 0.0;
+#pragma unroll
+        for (int j = 0; j < M; ++j) sc = fmax(sc, fabs(A[j * M + j]));
+        s_scale = sc;
+    }
+    __syncthreads();
+    const double scale = s_scale;
+    scale_out = scale;
+#pragma unroll 1
+    for (int j = 0; j < M; ++j) {
+        const double piv = A[j * M + j];
+        if (!isfinite(piv) || piv <= tol * scale) {
+            piv_out = piv;
+            return j;
+        }
+        const double rjj = sqrt(piv);
+        for (int k = j + 1 + tid; k < M; k += nthr) R[j * M + k] = A[j * M + k] / rjj;
+        if (tid == 0) {
+            R[j * M + j] = rjj;
+            s_rinv[j] = 1.0 / rjj;
+        }
+        __syncthreads();
+        const int L = M - j - 1;
+        for (int e = tid; e < L * L; e += nthr) {
+            const int i = j + 1 + e / L, k = j + 1 + e % L;
+            A[i * M + k] -= R[j * M + i] * R[j * M + k];
+        }
+        __syncthreads();
+    }
+    if (tid < M) {
+        const int c = tid;
+        double col[M];
+#pragma unroll
+        for (int i = M - 1; i >= 0; --i) {
+            double s = 0.0;
+#pragma unroll
+            for (int k = i + 1; k < M; ++k) s += (k <= c) ? R[i * M + k] * col[k] : 0.0;
+            col[i] = (i > c) ? 0.0 : (i == c) ? s_rinv[c] : -s * s_rinv[i];
+        }
+#pragma unroll
+        for (int i = 0; i < M; ++i) S[i * M + c] = col[i];
+    }
+    __syncthreads();
+    return -1;
+}
+
+// Cholesky + explicit inverse of the symmetric m x m matrix in A (smem,
+// overwritten): R, S = R^-1 into smem.  -1 or the failing column.
+__device__ inline int chol_inverse(double* A, double* R, double* S, int m, double tol, double& piv, double& scale) {
+    switch (m) {
+        case 8: return chol_inv_fixed<8>(A, R, S, tol, piv, scale);
+        case 16: return chol_inv_fixed<16>(A, R, S, tol, piv, scale);
+        case 32: return chol_inv_fixed<32>(A, R, S, tol, piv, scale);
+        default: {
+            const int fail = chol_rows(A, R, m, tol, piv, scale);
+            if (fail < 0) tri_inverse(R, S, m);
+            return fail;
+        }
+    }
+}
+
 __device__ inline void record_breakdown(EkcgCtrl* ctrl, int kind, int col, double piv, double scale, int iteration) {
     if (iteration <= 0) iteration = ctrl->k_done + 1;  // graph replay: iteration read on the device
     ctrl->brk_kind = kind;
@@ -117,12 +191,11 @@ __device__ inline void prechol_body(double* G, double* R, double* S, int m, doub
     __syncthreads();
     for (int e = tid; e < m * m; e += blockDim.x) G[e] = R[e];
     __syncthreads();
-    int fail = chol_rows(G, R, m, tol, piv, scale);
+    int fail = chol_inverse(G, R, S, m, tol, piv, scale);
     if (fail >= 0) {
         if (tid == 0) record_breakdown(ctrl, 2, fail, piv, scale, iteration);
         return;
     }
-    tri_inverse(R, S, m);
     for (int e = tid; e < m * m; e += blockDim.x) S0out[e] = S[e] / nrm[e / m];
 }
 
@@ -139,12 +212,11 @@ __device__ inline void cholinv_body(double* G, double* R, double* S, int m, doub
     __syncthreads();
     for (int e = tid; e < m * m; e += blockDim.x) G[e] = R[e];
     __syncthreads();
-    int fail = chol_rows(G, R, m, tol, piv, scale);
+    int fail = chol_inverse(G, R, S, m, tol, piv, scale);
     if (fail >= 0) {
         if (tid == 0) record_breakdown(ctrl, 2, fail, piv, scale, iteration);
         return;
     }
-    tri_inverse(R, S, m);
     for (int e = tid; e < m * m; e += blockDim.x) Sout[e] = S[e];
 }
 
@@ -199,6 +271,29 @@ __device__ inline void cta_sum_partials(const double* partials, int P, int len, 
     for (int j = tid; j < len; j += nthr) {
         double s = __ldcg(partials + j);
         for (int p = 1; p < P; ++p) s += __ldcg(partials + (long long)p * len + j);
+        out[j] = s;
+    }
+    __syncthreads();
+}
+
+// Deterministic high-MLP sum of P partial vectors by one CTA: thread j sums
+// p = 0..P-1 into 16 interleaved accumulators, then combines them in order.
+__device__ inline void cta_sum_partials_mlp(const double* partials, int P, int len, double* out) {
+    const int nthr = blockDim.x * blockDim.y;
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+    for (int j = tid; j < len; j += nthr) {
+        double acc[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = 0.0;
+        int p = 0;
+        for (; p + 16 <= P; p += 16) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] += __ldcg(partials + (long long)(p + q) * len + j);
+        }
+        for (int q = 0; p < P; ++p, ++q) acc[q] += __ldcg(partials + (long long)p * len + j);
+        double s = acc[0];
+#pragma unroll
+        for (int q = 1; q < 16; ++q) s += acc[q];
         out[j] = s;
     }
     __syncthreads();

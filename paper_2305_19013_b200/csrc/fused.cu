@@ -27,29 +27,6 @@ __host__ __device__ constexpr int pad_stride(int M) { return M == 8 ? 20 : M + 4
 
 constexpr int kFusedCtas = 148 * 2;
 
-// Deterministic high-MLP sum of P partial vectors by one CTA: thread j sums
-// p = 0..P-1 into 16 interleaved accumulators, then combines them in order.
-__device__ void cta_sum_partials_mlp(const double* partials, int P, int len, double* out) {
-    const int nthr = blockDim.x * blockDim.y;
-    const int tid = threadIdx.y * blockDim.x + threadIdx.x;
-    for (int j = tid; j < len; j += nthr) {
-        double acc[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) acc[q] = 0.0;
-        int p = 0;
-        for (; p + 16 <= P; p += 16) {
-#pragma unroll
-            for (int q = 0; q < 16; ++q) acc[q] += __ldcg(partials + (long long)(p + q) * len + j);
-        }
-        for (int q = 0; p < P; ++p, ++q) acc[q] += __ldcg(partials + (long long)p * len + j);
-        double s = acc[0];
-#pragma unroll
-        for (int q = 1; q < 16; ++q) s += acc[q];
-        out[j] = s;
-    }
-    __syncthreads();
-}
-
 // acc[ta][tb] += A^T B over the k-steps [k0, k1) (stride ks) of a row tile in
 // smem: A rows TA[r][a0 + .], B rows TB[r][b0 + .] with row stride lds.
 template <int NA, int NB>
@@ -500,6 +477,11 @@ extern "C" int ekcg_stencil_cholinv(const EkcgStencil* desc, const double* X, in
     EkcgCtrl* c = (EkcgCtrl*)ctrl;
     cudaStream_t st = as_stream(stream);
     n = s.row_end - s.row_begin;
+    if (launch_march_cholinv(s, uf, X, ldx, m, partials, counter, S, c, iteration, tol, finalize, kFusedCtas, st) ==
+        EKCG_OK) {
+        ++g_ekcg_launches;
+        return launch_status();
+    }
     switch (m) {
         case 8: rc = launch_stencil_cholinv<4, 8>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, finalize, st); break;
         case 16: rc = launch_stencil_cholinv<4, 16>(s, uf, n, X, ldx, partials, counter, S, c, iteration, tol, finalize, st); break;
@@ -526,6 +508,11 @@ extern "C" int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx
     cudaStream_t st = as_stream(stream);
     const bool aligned = (ldx % 2 == 0) && (ldy % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
+    if (launch_march_xr(s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k, kmax, stagnation_window,
+                        history, do_finish, rho2_out, kFusedCtas, st) == EKCG_OK) {
+        ++g_ekcg_launches;
+        return launch_status();
+    }
     int vec = 1;
     if (aligned && m % 4 == 0) vec = 4;
     else if (aligned && m % 2 == 0) vec = 2;

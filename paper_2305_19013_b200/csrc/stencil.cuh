@@ -243,3 +243,12 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
                      int m, const int* live, cudaStream_t st);
 extern int g_stencil_march;  // ekcg_tune key 3
 extern int g_march_variant;  // ekcg_tune key 4
+extern int g_march_fused;    // ekcg_tune key 9
+// Fused plane-marching kernels for m = 16 (stencil_march.cu); EKCG_EINVAL when they do not apply.
+int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, int m,
+                         double* partials, unsigned int* counter, double* S, EkcgCtrl* ctrl, int iteration, double tol,
+                         int finalize, int max_ctas, cudaStream_t st);
+int launch_march_xr(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy, int m,
+                    const double* alpha, double* x, double* r, double* partials, unsigned int* counter, EkcgCtrl* ctrl,
+                    int k, int kmax, int stag, double* history, int do_finish, double* rho2_out, int max_ctas,
+                    cudaStream_t st);

@@ -20,8 +20,11 @@
 #include "ekcg_b200.h"
 #include "stencil.cuh"
 #include "tma.cuh"
+#include "factor.cuh"
 
 namespace {
+
+using namespace ekcg_dev;
 
 // Tile shapes: 3-D TX x TY in (x, y); 2-D a TX segment of the x axis.  NS
 // stages; NS - 2 planes are loaded ahead of the one being computed.
@@ -39,6 +42,91 @@ struct March {
     static constexpr int MINB = (int)((227 * 1024) / (SMEM + 1024)) < 8 ? (int)((227 * 1024) / (SMEM + 1024)) : 8;
     static_assert(ITEMS % NT == 0, "items per thread");
 };
+
+// A X for one item: node (x0+ix, y0+iy) of plane w, columns 4 ig .. 4 ig+3 of
+// the chunk, from the staged planes pm / pc / pp (previous, current, next).
+// o[0..1] are columns 4 ig + ha (+1), o[2..3] columns 4 ig + hb (+1).
+template <class P>
+__device__ __forceinline__ void march_node(const EkcgStencil& s, const UniformFaces& uf, const double* pm,
+                                           const double* pc, const double* pp, int x0, int y0, int ix, int iy, int ig,
+                                           int w, unsigned nx, unsigned ny, unsigned nw, double (&o)[4], int& ha,
+                                           int& hb) {
+    constexpr int DIM = P::DIM, KC = P::KC;
+    const unsigned x = x0 + ix, y = y0 + iy;
+    const bool interior = x > 0 && x + 1 < nx && w > 0 && (unsigned)w + 1 < nw &&
+                          (DIM == 2 || (y > 0 && y + 1 < ny));
+    double v[7];
+    unsigned mk;
+    if (interior && s.kfield == nullptr) {
+        v[0] = -uf.fz; v[1] = -uf.fy; v[2] = -uf.fx; v[3] = uf.dint;
+        v[4] = -uf.fx; v[5] = -uf.fy; v[6] = -uf.fz;
+        mk = (DIM == 3) ? 0x7fu : 0x3eu;
+    } else {
+        mk = (DIM == 3) ? stencil_coef(s, uf, x, y, (unsigned)w, v)
+                        : stencil_coef(s, uf, x, (unsigned)w, 0u, v);
+    }
+    const int hc = ((iy + P::OY) * P::PX + ix + 1) * KC + 4 * ig;
+    // neighbour slices in entry order z-, y-, x-, diag, x+, y+, z+ (2-D: the march axis is y)
+    const double* nb[7];
+    if (DIM == 3) {
+        nb[0] = pm + hc; nb[1] = pc + hc - P::PX * KC; nb[2] = pc + hc - KC; nb[3] = pc + hc;
+        nb[4] = pc + hc + KC; nb[5] = pc + hc + P::PX * KC; nb[6] = pp + hc;
+    } else {
+        nb[0] = pc; nb[1] = pm + hc; nb[2] = pc + hc - KC; nb[3] = pc + hc;
+        nb[4] = pc + hc + KC; nb[5] = pp + hc; nb[6] = pc;
+    }
+    // the two 16-B halves of the item's 4 columns: for KC = 16 odd nodes
+    // take the upper 8 columns first, so a quarter warp (2 nodes x 4
+    // lanes) reads 128 distinct bytes per LDS.128 -- no bank conflicts
+    const int sw = (KC == 16) ? ((ix & 1) ? 8 : 0) : 0;
+    ha = (2 * ig + sw) % KC - 4 * ig;
+    hb = (2 * ig + KC / 2 + sw) % KC - 4 * ig;
+    if (interior) {
+        // all entries present: straight-line p0 + ((p1 + p2) + ...)
+        constexpr int e0 = (DIM == 3) ? 0 : 1, e1 = (DIM == 3) ? 6 : 5;
+        double p0[4], acc[4];
+        {
+            const double2 a = *reinterpret_cast<const double2*>(nb[e0] + ha);
+            const double2 b = *reinterpret_cast<const double2*>(nb[e0] + hb);
+            p0[0] = mul_rn(v[e0], a.x); p0[1] = mul_rn(v[e0], a.y);
+            p0[2] = mul_rn(v[e0], b.x); p0[3] = mul_rn(v[e0], b.y);
+        }
+        {
+            const double2 a = *reinterpret_cast<const double2*>(nb[e0 + 1] + ha);
+            const double2 b = *reinterpret_cast<const double2*>(nb[e0 + 1] + hb);
+            acc[0] = mul_rn(v[e0 + 1], a.x); acc[1] = mul_rn(v[e0 + 1], a.y);
+            acc[2] = mul_rn(v[e0 + 1], b.x); acc[3] = mul_rn(v[e0 + 1], b.y);
+        }
+#pragma unroll
+        for (int e = e0 + 2; e <= e1; ++e) {
+            const double2 a = *reinterpret_cast<const double2*>(nb[e] + ha);
+            const double2 b = *reinterpret_cast<const double2*>(nb[e] + hb);
+            acc[0] = add_rn(acc[0], mul_rn(v[e], a.x)); acc[1] = add_rn(acc[1], mul_rn(v[e], a.y));
+            acc[2] = add_rn(acc[2], mul_rn(v[e], b.x)); acc[3] = add_rn(acc[3], mul_rn(v[e], b.y));
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = add_rn(p0[j], acc[j]);
+    } else {
+        double p0[4] = {0.0, 0.0, 0.0, 0.0}, acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int seen = 0;
+#pragma unroll
+        for (int e = 0; e < 7; ++e) {
+            if (!(mk & (1u << e))) continue;
+            const double2 a = *reinterpret_cast<const double2*>(nb[e] + ha);
+            const double2 b = *reinterpret_cast<const double2*>(nb[e] + hb);
+            const double pr[4] = {mul_rn(v[e], a.x), mul_rn(v[e], a.y), mul_rn(v[e], b.x), mul_rn(v[e], b.y)};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                if (seen == 0) p0[j] = pr[j];
+                else if (seen == 1) acc[j] = pr[j];
+                else acc[j] = add_rn(acc[j], pr[j]);
+            }
+            ++seen;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) o[j] = add_rn(p0[j], acc[j]);
+    }
+}
 
 template <class P>
 __global__ void __launch_bounds__(P::NT, P::MINB)
@@ -112,80 +200,9 @@ stencil_march_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil s, Un
         for (int it = 0; it < P::IPT; ++it) {
             if (!act[it]) continue;
             const unsigned x = x0 + ix[it], y = y0 + iy[it];
-            const bool interior = x > 0 && x + 1 < nx && w > 0 && (unsigned)w + 1 < nw &&
-                                  (DIM == 2 || (y > 0 && y + 1 < ny));
-            double v[7];
-            unsigned mk;
-            if (interior && s.kfield == nullptr) {
-                v[0] = -uf.fz; v[1] = -uf.fy; v[2] = -uf.fx; v[3] = uf.dint;
-                v[4] = -uf.fx; v[5] = -uf.fy; v[6] = -uf.fz;
-                mk = (DIM == 3) ? 0x7fu : 0x3eu;
-            } else {
-                mk = (DIM == 3) ? stencil_coef(s, uf, x, y, (unsigned)w, v)
-                                : stencil_coef(s, uf, x, (unsigned)w, 0u, v);
-            }
-            const int hc = ((iy[it] + P::OY) * P::PX + ix[it] + 1) * KC + 4 * ig[it];
-            // neighbour slices in entry order z-, y-, x-, diag, x+, y+, z+ (2-D: the march axis is y)
-            const double* nb[7];
-            if (DIM == 3) {
-                nb[0] = pm + hc; nb[1] = pc + hc - P::PX * KC; nb[2] = pc + hc - KC; nb[3] = pc + hc;
-                nb[4] = pc + hc + KC; nb[5] = pc + hc + P::PX * KC; nb[6] = pp + hc;
-            } else {
-                nb[0] = pc; nb[1] = pm + hc; nb[2] = pc + hc - KC; nb[3] = pc + hc;
-                nb[4] = pc + hc + KC; nb[5] = pp + hc; nb[6] = pc;
-            }
-            // the two 16-B halves of the item's 4 columns: for KC = 16 odd nodes
-            // take the upper 8 columns first, so a quarter warp (2 nodes x 4
-            // lanes) reads 128 distinct bytes per LDS.128 -- no bank conflicts
-            const int sw = (KC == 16) ? ((ix[it] & 1) ? 8 : 0) : 0;
-            const int ha = (2 * ig[it] + sw) % KC - 4 * ig[it];
-            const int hb = (2 * ig[it] + KC / 2 + sw) % KC - 4 * ig[it];
             double o[4];
-            if (interior) {
-                // all entries present: straight-line p0 + ((p1 + p2) + ...)
-                constexpr int e0 = (DIM == 3) ? 0 : 1, e1 = (DIM == 3) ? 6 : 5;
-                double p0[4], acc[4];
-                {
-                    const double2 a = *reinterpret_cast<const double2*>(nb[e0] + ha);
-                    const double2 b = *reinterpret_cast<const double2*>(nb[e0] + hb);
-                    p0[0] = mul_rn(v[e0], a.x); p0[1] = mul_rn(v[e0], a.y);
-                    p0[2] = mul_rn(v[e0], b.x); p0[3] = mul_rn(v[e0], b.y);
-                }
-                {
-                    const double2 a = *reinterpret_cast<const double2*>(nb[e0 + 1] + ha);
-                    const double2 b = *reinterpret_cast<const double2*>(nb[e0 + 1] + hb);
-                    acc[0] = mul_rn(v[e0 + 1], a.x); acc[1] = mul_rn(v[e0 + 1], a.y);
-                    acc[2] = mul_rn(v[e0 + 1], b.x); acc[3] = mul_rn(v[e0 + 1], b.y);
-                }
-#pragma unroll
-                for (int e = e0 + 2; e <= e1; ++e) {
-                    const double2 a = *reinterpret_cast<const double2*>(nb[e] + ha);
-                    const double2 b = *reinterpret_cast<const double2*>(nb[e] + hb);
-                    acc[0] = add_rn(acc[0], mul_rn(v[e], a.x)); acc[1] = add_rn(acc[1], mul_rn(v[e], a.y));
-                    acc[2] = add_rn(acc[2], mul_rn(v[e], b.x)); acc[3] = add_rn(acc[3], mul_rn(v[e], b.y));
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) o[j] = add_rn(p0[j], acc[j]);
-            } else {
-                double p0[4] = {0.0, 0.0, 0.0, 0.0}, acc[4] = {0.0, 0.0, 0.0, 0.0};
-                int seen = 0;
-#pragma unroll
-                for (int e = 0; e < 7; ++e) {
-                    if (!(mk & (1u << e))) continue;
-                    const double2 a = *reinterpret_cast<const double2*>(nb[e] + ha);
-                    const double2 b = *reinterpret_cast<const double2*>(nb[e] + hb);
-                    const double pr[4] = {mul_rn(v[e], a.x), mul_rn(v[e], a.y), mul_rn(v[e], b.x), mul_rn(v[e], b.y)};
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        if (seen == 0) p0[j] = pr[j];
-                        else if (seen == 1) acc[j] = pr[j];
-                        else acc[j] = add_rn(acc[j], pr[j]);
-                    }
-                    ++seen;
-                }
-#pragma unroll
-                for (int j = 0; j < 4; ++j) o[j] = add_rn(p0[j], acc[j]);
-            }
+            int ha, hb;
+            march_node<P>(s, uf, pm, pc, pp, x0, y0, ix[it], iy[it], ig[it], w, nx, ny, nw, o, ha, hb);
             const long long row = (DIM == 3) ? ((long long)w * ny + y) * nx + x : (long long)w * nx + x;
             double* yr = Y + row * ldy + c0 + 4 * ig[it];
             *reinterpret_cast<double2*>(yr + ha) = make_double2(o[0], o[1]);
@@ -211,12 +228,10 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 }
 
 template <class P>
-int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy, int m,
-                 int wb, int we, const int* live, cudaStream_t st) {
+bool make_plane_map(const EkcgStencil& s, const double* X, int ldx, int m, CUtensorMap& map) {
     constexpr int DIM = P::DIM, KC = P::KC;
     auto encode = encode_fn();
-    if (encode == nullptr) return EKCG_EINVAL;
-    CUtensorMap map;
+    if (encode == nullptr) return false;
     cuuint64_t dims[4], strides[3];
     cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
     dims[0] = (cuuint64_t)m;
@@ -236,10 +251,17 @@ int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, 
         strides[1] = strides[0] * s.nx;
         box[2] = 1;
     }
-    CUresult r = encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, DIM + 1, const_cast<double*>(X), dims, strides, box,
-                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) return EKCG_EINVAL;
+    return encode(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, DIM + 1, const_cast<double*>(X), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <class P>
+int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy, int m,
+                 int wb, int we, const int* live, cudaStream_t st) {
+    constexpr int DIM = P::DIM, KC = P::KC;
+    CUtensorMap map;
+    if (!make_plane_map<P>(s, X, ldx, m, map)) return EKCG_EINVAL;
 
     static int resident = 0;
     if (resident == 0) {
@@ -270,6 +292,262 @@ int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, 
     return EKCG_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Fused plane-marching kernels for 16-column blocks (one column chunk), a
+// persistent grid walking (tile, plane-chunk) work items:
+//   EPI_GRAM: G = X^T (A X) -- A X goes to a shared tile, never to HBM; the
+//             DMMA consumes X from the staged plane and A X from the tile --
+//             then the last CTA sums the CTA partials (fixed order) and
+//             factors G (A-CholQR: S = chol(sym G)^-1), or stores G.
+//   EPI_XR:   Y = A X written; x += X alpha, r -= Y alpha, |r|^2 partials;
+//             the last CTA finishes the iteration (or stores |r|^2).
+// ---------------------------------------------------------------------------
+constexpr int EPI_GRAM = 1, EPI_XR = 2;
+
+struct FusedArgs {
+    double* partials;
+    unsigned int* counter;
+    EkcgCtrl* ctrl;
+    int iteration;
+    double tol;
+    int finalize;
+    double* out;  // S (finalize) or G
+    // xr
+    double* Y;
+    int ldy;
+    const double* alpha;
+    double* x;
+    double* r;
+    int k, kmax, stag;
+    double* history;
+    int do_finish;
+    double* rho2_out;
+};
+
+template <class P, int EPI>
+__global__ void __launch_bounds__(P::NT, 2)
+stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil s, UniformFaces uf, int w_begin,
+                           int w_end, int wchunk, int items, FusedArgs fa) {
+    if (fa.ctrl->live == 0) return;
+    constexpr int DIM = P::DIM, KC = P::KC, kNS = P::NS, kAhead = P::AHEAD, NODES = P::TX * P::TY;
+    static_assert(KC == 16 && P::IPT == 1 && P::NT == 256 && NODES == 64, "16 columns, 64-node tiles");
+    extern __shared__ __align__(128) double smem[];
+    __shared__ __align__(8) unsigned long long bar[kNS];
+    __shared__ __align__(16) double sa[16];
+    double* tileY = smem + kNS * P::STAGE;  // [NODES][16] A X of the current plane (EPI_GRAM)
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned nx = s.nx, ny = s.ny;
+    const unsigned nw = (DIM == 3) ? s.nz : ny;
+    const unsigned tiles_x = (nx + P::TX - 1) / P::TX;
+    const int planes = w_end - w_begin;
+    const int wchunks = (planes + wchunk - 1) / wchunk;
+    if (tid == 0) {
+#pragma unroll
+        for (int q = 0; q < kNS; ++q) mbar_init(&bar[q], 1);
+        mbar_fence_init();
+    }
+    if (EPI == EPI_XR && tid < 16) sa[tid] = fa.alpha[tid];
+    __syncthreads();
+
+    const int nd = tid >> 2, ig = tid & 3;
+    const int ix = nd % P::TX, iy = nd / P::TX;
+    const int lr = lane & 3, lc = lane >> 2;
+    double gacc[2][2][2] = {{{0.0, 0.0}, {0.0, 0.0}}, {{0.0, 0.0}, {0.0, 0.0}}};
+    double sq = 0.0;
+    long long qg = 0;  // planes issued by this CTA so far (ring position and mbarrier phase)
+
+    for (int item = blockIdx.x; item < items; item += gridDim.x) {
+        const int tile = item / wchunks, wc = item % wchunks;
+        const int x0 = (int)((tile % tiles_x) * P::TX);
+        const int y0 = (DIM == 3) ? (int)((tile / tiles_x) * P::TY) : 0;
+        const int wb = w_begin + wc * wchunk;
+        const int we = min(w_end, wb + wchunk);
+        const int nq = we - wb + 2;
+        __syncthreads();  // the previous item's reads are done before its stages are refilled
+        auto issue = [&](int q) {
+            const long long g = qg + q;
+            const int slot = (int)(g % kNS);
+            mbar_expect_tx(&bar[slot], (unsigned)(P::BOX * sizeof(double)));
+            const int z = wb - 1 + q;
+            if (DIM == 3) tma_load_4d(smem + slot * P::STAGE, &tmap, &bar[slot], 0, x0 - 1, y0 - 1, z);
+            else tma_load_3d(smem + slot * P::STAGE, &tmap, &bar[slot], 0, x0 - 1, z);
+        };
+        if (tid == 0)
+            for (int q = 0; q <= kAhead && q < nq; ++q) issue(q);
+        const bool act = (x0 + ix < (int)nx) && (DIM == 2 || y0 + iy < (int)ny);
+        for (int w = wb; w < we; ++w) {
+            const int q = w - wb + 1;
+            if (tid == 0) {
+                if (w == wb) {
+                    mbar_wait(&bar[(qg + q - 1) % kNS], (unsigned)(((qg + q - 1) / kNS) & 1));
+                    mbar_wait(&bar[(qg + q) % kNS], (unsigned)(((qg + q) / kNS) & 1));
+                }
+                mbar_wait(&bar[(qg + q + 1) % kNS], (unsigned)(((qg + q + 1) / kNS) & 1));
+            }
+            __syncthreads();
+            if (tid == 0 && q + kAhead < nq) issue(q + kAhead);
+            const double* pm = smem + ((qg + q - 1) % kNS) * P::STAGE;
+            const double* pc = smem + ((qg + q) % kNS) * P::STAGE;
+            const double* pp = smem + ((qg + q + 1) % kNS) * P::STAGE;
+            double o[4] = {0.0, 0.0, 0.0, 0.0};
+            int ha = 0, hb = 0;
+            if (act) march_node<P>(s, uf, pm, pc, pp, x0, y0, ix, iy, ig, w, nx, ny, nw, o, ha, hb);
+            else {
+                const int sw = (ix & 1) ? 8 : 0;
+                ha = (2 * ig + sw) % KC - 4 * ig;
+                hb = (2 * ig + KC / 2 + sw) % KC - 4 * ig;
+            }
+            if (EPI == EPI_GRAM) {
+                double* ty = tileY + nd * KC + 4 * ig;
+                *reinterpret_cast<double2*>(ty + ha) = make_double2(o[0], o[1]);
+                *reinterpret_cast<double2*>(ty + hb) = make_double2(o[2], o[3]);
+                __syncthreads();
+                // G += X^T (A X) over the 64 nodes: 16 k-steps, two per warp; lane (i, k) reads
+                // columns 2i, 2i+1 of node k (interleaved tiles t: column 2i + t)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int node = 4 * (warp + 8 * h) + lr;
+                    const int hx = node % P::TX, hy = node / P::TX;
+                    const double2 a = *reinterpret_cast<const double2*>(
+                        pc + ((hy + P::OY) * P::PX + hx + 1) * KC + 2 * lc);
+                    const double2 b = *reinterpret_cast<const double2*>(tileY + node * KC + 2 * lc);
+                    dmma_8x8x4(gacc[0][0], a.x, b.x);
+                    dmma_8x8x4(gacc[0][1], a.x, b.y);
+                    dmma_8x8x4(gacc[1][0], a.y, b.x);
+                    dmma_8x8x4(gacc[1][1], a.y, b.y);
+                }
+            } else {
+                // every lane takes part in the shuffles; inactive nodes contribute zeros
+                const unsigned x = x0 + ix, y = y0 + iy;
+                const long long row = (DIM == 3) ? ((long long)w * ny + y) * nx + x : (long long)w * nx + x;
+                double xv = 0.0, rv = 0.0, dx = 0.0, dr = 0.0;
+                if (act) {
+                    if (ig == 0) {
+                        xv = fa.x[row];
+                        rv = fa.r[row];
+                    }
+                    double* yr = fa.Y + row * fa.ldy + 4 * ig;
+                    *reinterpret_cast<double2*>(yr + ha) = make_double2(o[0], o[1]);
+                    *reinterpret_cast<double2*>(yr + hb) = make_double2(o[2], o[3]);
+                    const double* xc = pc + ((iy + P::OY) * P::PX + ix + 1) * KC + 4 * ig;
+                    const double2 w0 = *reinterpret_cast<const double2*>(xc + ha);
+                    const double2 w1 = *reinterpret_cast<const double2*>(xc + hb);
+                    const int ca = 4 * ig + ha, cb = 4 * ig + hb;
+                    dx = w0.x * sa[ca] + w0.y * sa[ca + 1] + w1.x * sa[cb] + w1.y * sa[cb + 1];
+                    dr = o[0] * sa[ca] + o[1] * sa[ca + 1] + o[2] * sa[cb] + o[3] * sa[cb + 1];
+                }
+                dx += __shfl_xor_sync(0xffffffffu, dx, 1);
+                dr += __shfl_xor_sync(0xffffffffu, dr, 1);
+                dx += __shfl_xor_sync(0xffffffffu, dx, 2);
+                dr += __shfl_xor_sync(0xffffffffu, dr, 2);
+                if (act && ig == 0) {
+                    fa.x[row] = xv + dx;
+                    const double rn = rv - dr;
+                    fa.r[row] = rn;
+                    sq += rn * rn;
+                }
+            }
+        }
+        qg += nq;
+    }
+
+    // CTA partial, fixed order, then the last CTA's epilogue
+    __syncthreads();
+    if (EPI == EPI_GRAM) {
+        double* red = smem;  // [8 warps][256]
+#pragma unroll
+        for (int ta = 0; ta < 2; ++ta)
+#pragma unroll
+            for (int tb = 0; tb < 2; ++tb)
+#pragma unroll
+                for (int e = 0; e < 2; ++e)
+                    red[warp * 256 + (2 * lc + ta) * 16 + 2 * (2 * lr + e) + tb] = gacc[ta][tb][e];
+        __syncthreads();
+        {
+            double v = red[tid];
+#pragma unroll
+            for (int w = 1; w < 8; ++w) v += red[w * 256 + tid];
+            fa.partials[(long long)blockIdx.x * 256 + tid] = v;
+        }
+        if (last_cta_arrive(fa.counter)) {
+            double* Gm = smem + 8 * 256;
+            cta_sum_partials_mlp(fa.partials, gridDim.x, 256, Gm);
+            if (fa.finalize) cholinv_body(Gm, Gm + 256, Gm + 512, 16, fa.out, fa.ctrl, fa.iteration, fa.tol);
+            else
+                for (int e = tid; e < 256; e += 256) fa.out[e] = Gm[e];
+        }
+    } else {
+        __shared__ double wsum[8];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) wsum[warp] = sq;
+        __syncthreads();
+        if (tid == 0) {
+            double t = wsum[0];
+            for (int w = 1; w < 8; ++w) t += wsum[w];
+            fa.partials[blockIdx.x] = t;
+        }
+        if (last_cta_arrive(fa.counter)) {
+            __shared__ double tot;
+            if (tid < 32) {
+                double acc = 0.0;
+                for (int p = tid; p < (int)gridDim.x; p += 32) acc += __ldcg(fa.partials + p);
+                for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (tid == 0) tot = acc;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                if (fa.do_finish) finish_body(fa.ctrl, tot, fa.k, fa.kmax, fa.stag, fa.history);
+                else *fa.rho2_out = tot;
+            }
+        }
+    }
+}
+
+template <class P, int EPI>
+int launch_march_fused(const EkcgStencil& s, const UniformFaces& uf, const double* X, int max_ctas,
+                       const FusedArgs& fa, cudaStream_t st) {
+    constexpr int DIM = P::DIM;
+    const long long plane = (DIM == 3) ? (long long)s.nx * s.ny : (long long)s.nx;
+    if (s.row_begin % plane != 0 || s.row_end % plane != 0) return EKCG_EINVAL;
+    const int wb = (int)(s.row_begin / plane), we = (int)(s.row_end / plane);
+    CUtensorMap map;
+    if (!make_plane_map<P>(s, X, 16, 16, map)) return EKCG_EINVAL;
+    constexpr size_t smem = P::SMEM + sizeof(double) * 64 * 16;
+    static_assert(P::SMEM >= sizeof(double) * 11 * 256, "reduction scratch fits the stages");
+    static int resident = 0;
+    if (resident == 0) {
+        auto fn = stencil_march_fused_kernel<P, EPI>;
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
+            cudaGetLastError();
+            return EKCG_EINVAL;
+        }
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P::NT, smem) != cudaSuccess || occ < 1) {
+            cudaGetLastError();
+            occ = 1;
+        }
+        int dev = 0, sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        resident = occ * sms;
+    }
+    const long long tiles = (DIM == 3) ? (long long)((s.nx + P::TX - 1) / P::TX) * ((s.ny + P::TY - 1) / P::TY)
+                                       : (long long)((s.nx + P::TX - 1) / P::TX);
+    int grid = resident < max_ctas ? resident : max_ctas;
+    // plane chunks: about one work item per resident CTA, marches of >= 4 planes
+    const int planes = we - wb;
+    long long wchunks = (grid + tiles - 1) / tiles;
+    if (wchunks > planes / 4) wchunks = planes / 4;
+    if (wchunks < 1) wchunks = 1;
+    const int wchunk = (int)((planes + wchunks - 1) / wchunks);
+    wchunks = (planes + wchunk - 1) / wchunk;
+    const long long items = tiles * wchunks;
+    if (items < grid) grid = (int)items;
+    stencil_march_fused_kernel<P, EPI><<<grid, P::NT, smem, st>>>(map, s, uf, wb, we, wchunk, (int)items, fa);
+    return EKCG_OK;
+}
+
 }  // namespace
 
 // Launch the plane-marching kernel when it applies (m % 4 == 0, 16-byte
@@ -291,9 +569,9 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
                 case 2: return launch_march<March<3, 16, 16, 4, 8>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
                 case 3: return launch_march<March<3, 16, 32, 4, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
                 case 4: return launch_march<March<3, 16, 16, 4, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                case 5: return launch_march<March<3, 16, 16, 4, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
+                case 5: return launch_march<March<3, 16, 16, 8, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
                 case 6: return launch_march<March<3, 16, 32, 8, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                default: return launch_march<March<3, 16, 16, 8, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
+                default: return launch_march<March<3, 16, 16, 4, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
             }
         }
         if (kc == 8) return launch_march<March<3, 8, 16, 8, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
@@ -302,4 +580,50 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
     if (kc == 16) return launch_march<March<2, 16, 64, 1, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
     if (kc == 8) return launch_march<March<2, 8, 128, 1, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
     return launch_march<March<2, 4, 128, 1, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
+}
+
+// Fused plane-marching kernels for m = 16 (EKCG_EINVAL when they do not apply:
+// the caller takes the row-parallel fused kernels).
+int g_march_fused = 1;  // ekcg_tune key 9
+
+int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, int m,
+                         double* partials, unsigned int* counter, double* S, EkcgCtrl* ctrl, int iteration, double tol,
+                         int finalize, int max_ctas, cudaStream_t st) {
+    if (!g_march_fused || m != 16 || ldx != 16 || (reinterpret_cast<uintptr_t>(X) & 15)) return EKCG_EINVAL;
+    FusedArgs fa{};
+    fa.partials = partials;
+    fa.counter = counter;
+    fa.ctrl = ctrl;
+    fa.iteration = iteration;
+    fa.tol = tol;
+    fa.finalize = finalize;
+    fa.out = S;
+    if (s.dim == 3) return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
+    return launch_march_fused<March<2, 16, 64, 1, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
+}
+
+int launch_march_xr(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy, int m,
+                    const double* alpha, double* x, double* r, double* partials, unsigned int* counter, EkcgCtrl* ctrl,
+                    int k, int kmax, int stag, double* history, int do_finish, double* rho2_out, int max_ctas,
+                    cudaStream_t st) {
+    if (!g_march_fused || m != 16 || ldx != 16 || ldy % 2 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) ||
+        (reinterpret_cast<uintptr_t>(Y) & 15))
+        return EKCG_EINVAL;
+    FusedArgs fa{};
+    fa.partials = partials;
+    fa.counter = counter;
+    fa.ctrl = ctrl;
+    fa.Y = Y;
+    fa.ldy = ldy;
+    fa.alpha = alpha;
+    fa.x = x;
+    fa.r = r;
+    fa.k = k;
+    fa.kmax = kmax;
+    fa.stag = stag;
+    fa.history = history;
+    fa.do_finish = do_finish;
+    fa.rho2_out = rho2_out;
+    if (s.dim == 3) return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
+    return launch_march_fused<March<2, 16, 64, 1, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
 }

@@ -13,8 +13,8 @@ cfg = pk.SolverConfig(**prob.solver_kwargs)
 op = prob.stencil()
 b = torch.as_tensor(prob.b, device='cuda')
 timer = bench.KernelTimer(torch, ["hist_gram", "hist_update"])
-variants = [("none", set()), ("all", {"prechol", "cholinv", "vec", "xr"}), ("cholinv", {"cholinv"}),
-            ("vec", {"vec"}), ("xr", {"xr"}), ("prechol", {"prechol"}), ("default", None)]
+variants = [("none", set()), ("cholinv+vec", {"cholinv", "vec"}), ("vec+xr", {"vec", "xr"}),
+            ("vec", {"vec"}), ("default", None)]
 for name, fuse in variants:
     for timed in (False,):
         ms = []

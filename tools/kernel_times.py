@@ -87,8 +87,10 @@ def fused_times():
     from paper_2305_19013_b200.operators import StencilOperator as SO
     import ctypes
     res = {}
-    for m, shape in ((16, (64, 64, 64)), (32, (128, 128, 128)), (64, (256, 256, 128))):
-        n = shape[0] * shape[1] * shape[2]
+    for m, shape in ((16, (64, 64, 64)), (16, (128, 128, 128)), (16, (512, 512))):
+        n = 1
+        for v in shape:
+            n *= v
         op = SO(shape, 1.0)
         X = torch.randn(n * m, dtype=torch.float64, device=dev)
         Y = torch.empty_like(X)
@@ -102,6 +104,7 @@ def fused_times():
         G = torch.empty(m * m, dtype=torch.float64, device=dev)
         hist = torch.zeros(16, dtype=torch.float64, device=dev)
         rho2 = torch.zeros(1, dtype=torch.float64, device=dev)
+        _lib.call("ekcg_tune", 9, int(sys.argv[-1]) if sys.argv[-1] in ("0", "1") else 1)
         tg = timeit(lambda: _lib.call("ekcg_stencil_cholinv", op.desc_ref(), X.data_ptr(), m, m, part.data_ptr(),
                                       cnt.data_ptr(), G.data_ptr(), ctrl.data_ptr(), 1, 1e-14, 0, st))
         tx = timeit(lambda: _lib.call("ekcg_stencil_xr", op.desc_ref(), X.data_ptr(), m, Y.data_ptr(), m, m,
@@ -110,7 +113,7 @@ def fused_times():
         ts = timeit(lambda: op.apply(X, m, Y, m, m))
         res[f"m{m}"] = {"stencil_cholinv_GBs": 8 * n * m / tg / 1e9, "stencil_xr_GBs": (16 * n * m + 32 * n) / tx / 1e9,
                         "stencil_GBs": 16 * n * m / ts / 1e9}
-        print(f"m{m}", {k: round(v) for k, v in res[f"m{m}"].items()}, flush=True)
+        print(f"m{m} {shape}", {k: round(v) for k, v in res[f"m{m}"].items()}, flush=True)
     return res
 
 
