@@ -32,7 +32,11 @@ extern "C" {
  * row-indexed pointer passed with a stencil descriptor is addressed by GLOBAL
  * row: element (i, c) of X is X[i*ldx + c] for the rows the stencil touches,
  * i.e. [row_begin - nx*ny, row_end + nx*ny) in 3-D -- a row shard passes a
- * base pointer shifted by its first row (halo planes included). */
+ * base pointer shifted by its first row (halo planes included).
+ * kself (optional, may be NULL): per tile, 2*k*k/(k+k) evaluated left to right
+ * in IEEE fp64 (the harmonic mean of a tile with itself, bitwise what the
+ * kernels would compute); faces between two nodes of one tile use it instead
+ * of a division. */
 typedef struct EkcgStencil {
     int dim;
     int nx, ny, nz;
@@ -42,6 +46,7 @@ typedef struct EkcgStencil {
     int fx, fy;
     double kconst;
     long long row_begin, row_end;
+    const double* kself;
 } EkcgStencil;
 
 /* ---- sparse operator and T^t split ------------------------------------ */

@@ -72,6 +72,7 @@ class EkcgStencil(ctypes.Structure):
         ("fx", c_int), ("fy", c_int),
         ("kconst", c_double),
         ("row_begin", c_longlong), ("row_end", c_longlong),
+        ("kself", c_void_p),
     ]
 
 

@@ -101,6 +101,11 @@ class StencilOperator:
             self.field_host = field
             self.field = torch.from_numpy(field.reshape(-1)).to(self.device)
             desc.kfield = self.field.data_ptr()
+            # harmonic mean of each tile with itself, 2*k*k/(k+k) left to right
+            # (generators.py:45 with ka = kb): same-tile faces skip the division
+            self.kself = torch.from_numpy(np.ascontiguousarray(2.0 * field * field / (field + field)).reshape(-1)).to(
+                self.device)
+            desc.kself = self.kself.data_ptr()
             desc.tx, desc.ty = tile[0], tile[1]
             desc.tz = tile[2] if self.dim == 3 else 1
             desc.fx, desc.fy = need[0], need[1]
