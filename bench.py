@@ -285,6 +285,8 @@ def run_ours(args):
     barrier()
     launches = _lib.query("ekcg_launch_count") - launches0
     clk = clocks.stop()
+    if rank == 0:
+        print(f"[bench] step ms: {[round(v, 2) for v in step_ms]}", file=sys.stderr)
 
     tot_ms = sum(step_ms)
     if world > 1:

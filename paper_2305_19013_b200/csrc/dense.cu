@@ -252,11 +252,24 @@ int gram_chunks(long long n, int d, int m1, int m2) {
     GramFn fn = select_gram(d, m1, m2, gb);
     const long long groups = (d + gb - 1) / gb;
     if (m1 == 16 && m2 == 16 && g_gram_stream && g_gram_target <= 0) {
-        // streamed Gram: one CTA per SM with long row ranges, one wave
-        long long p = (groups >= 148) ? 1 : 148 / groups;
-        const long long max_p = (n + 255) / 256;
-        if (p > max_p) p = max_p;
-        return (int)(p < 1 ? 1 : p);
+        // streamed Gram: one CTA per SM with long row ranges.  Pick the chunk
+        // count whose CTA total fills its last wave best (equal work per CTA),
+        // preferring fewer chunks; at least 1024 rows per chunk.
+        long long pmax = (n + 1023) / 1024;
+        const long long cap = (4 * 148 + groups - 1) / groups;
+        if (pmax > cap) pmax = cap;
+        if (pmax < 1) pmax = 1;
+        long long best = 1;
+        double best_eff = 0.0;
+        for (long long p = 1; p <= pmax; ++p) {
+            const long long ctas = p * groups;
+            const double eff = (double)ctas / (148.0 * (double)((ctas + 147) / 148));
+            if (eff > best_eff + 0.01) {
+                best_eff = eff;
+                best = p;
+            }
+        }
+        return (int)best;
     }
     long long target = g_gram_target;
     if (target <= 0) {
