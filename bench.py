@@ -282,6 +282,7 @@ def run_ours(args):
         reps.append(rep)
         dgram.extend(kd for kd in eng.launch_k if kd[0] <= rep.iterations)
         n_rows = eng.n  # local rows on a shard
+        eng = None  # release the solve's blocks before the next step allocates its own
     barrier()
     launches = _lib.query("ekcg_launch_count") - launches0
     clk = clocks.stop()

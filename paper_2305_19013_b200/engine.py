@@ -123,6 +123,7 @@ class DeviceEngine:
         # launches it replaces (15 ms per 130-iteration solve without graphs).
         self.use_graphs = False
         self._capturing = False
+        self._slab, self._slab_off = None, 0
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -284,9 +285,25 @@ class DeviceEngine:
             qbuf, aqbuf = self.slots[slot]
         else:
             slot = -1
-            f64 = dict(dtype=torch.float64, device=self.device)
-            qbuf, aqbuf = torch.empty(n * width, **f64), torch.empty(n * width, **f64)
+            qbuf, aqbuf = self._carve(n * width), self._carve(n * width)
         return _Block(qbuf, aqbuf, width, slot)
+
+    def _carve(self, numel):
+        """A fresh n x width block for full retention, carved from slabs of about
+        1 GiB: one allocation per slab instead of two per iteration, so a cold
+        caching allocator costs a few cudaMalloc calls per solve, not hundreds.
+        Views start on 256-B boundaries; blocks of >= 128 MiB are allocated alone."""
+        f64 = dict(dtype=torch.float64, device=self.device)
+        if numel * 8 >= (1 << 27):
+            return torch.empty(numel, **f64)
+        span = (numel + 31) // 32 * 32
+        if self._slab is None or self._slab_off + span > self._slab.numel():
+            per = max(1, (1 << 30) // (span * 8))
+            self._slab = torch.empty(per * span, **f64)
+            self._slab_off = 0
+        v = self._slab[self._slab_off:self._slab_off + numel]
+        self._slab_off += span
+        return v
 
     def _append(self, blk):
         self.retained.append(blk)

@@ -64,8 +64,9 @@ def main():
             e1.synchronize()
             ms = e0.elapsed_time(e1)
             if best is None or ms < best[0]:
-                best = (ms, rep, eng)
-        ms, rep, eng = best
+                best = (ms, rep, bool(eng.lean))
+            del eng, x  # the next repeat reuses the cached blocks
+        ms, rep, lean = best
         secs = ms / 1e3
         rel_true = rep.true_residual / float(np.linalg.norm(prob.b))
         t_hbm = rep.model_bytes / (hbm * 1e9)
@@ -76,7 +77,7 @@ def main():
             "it_per_s": rep.iterations / secs if secs else None,
             "rel_residual": float(rep.residual_history[-1] / rep.residual_history[0]),
             "rel_true_residual": rel_true, "relative_error": rep.relative_error,
-            "peak_block_vectors": rep.peak_block_vectors, "lean": bool(eng.lean),
+            "peak_block_vectors": rep.peak_block_vectors, "lean": lean,
             "model_GB": rep.model_bytes / 1e9, "model_TF": rep.model_flops / 1e12,
             "achieved_GBs": rep.model_bytes / secs / 1e9, "hbm_frac": t_hbm / secs,
             "fp64_frac": t_fp / secs, "roofline_frac": max(t_hbm, t_fp) / secs,
@@ -84,7 +85,7 @@ def main():
             "history_head": [float(v) for v in rep.residual_history[:6]],
         }
         print(json.dumps(line), flush=True)
-        del eng, rep, best, x, b, op, prob
+        del rep, best, b, op, prob
         torch.cuda.empty_cache()
         torch.cuda.reset_peak_memory_stats()
 
