@@ -42,6 +42,7 @@ extern int g_march_fused;
 
 int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
+long long g_march_min_work = 1LL << 21;  // smaller grids take the row-parallel stencil kernels
 int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
 int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
 namespace {
@@ -784,6 +785,10 @@ extern "C" int ekcg_tune(int key, long long value) {
     }
     if (key == 3 && value >= 0 && value <= 1) {
         g_stencil_march = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 12 && value >= 0) {
+        g_march_min_work = value;
         return EKCG_OK;
     }
     if (key == 9 && value >= 0 && value <= 1) {

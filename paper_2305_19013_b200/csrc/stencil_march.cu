@@ -26,6 +26,7 @@ namespace {
 
 using namespace ekcg_dev;
 
+
 // Tile shapes: 3-D TX x TY in (x, y); 2-D a TX segment of the x axis.  NS
 // stages; NS - 2 planes are loaded ahead of the one being computed.
 template <int DIM_, int KC_, int TX_, int TY_, int NS_>
@@ -560,6 +561,9 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
         return EKCG_EINVAL;
     const long long plane = (s.dim == 3) ? (long long)s.nx * s.ny : (long long)s.nx;
     if (s.row_begin % plane != 0 || s.row_end % plane != 0) return EKCG_EINVAL;
+    // small grids: the march is latency-bound (a few CTAs, serial plane steps);
+    // the row-parallel kernel finishes sooner
+    if ((s.row_end - s.row_begin) * (long long)m < g_march_min_work) return EKCG_EINVAL;
     const int wb = (int)(s.row_begin / plane), we = (int)(s.row_end / plane);
     const int kc = (m % 16 == 0) ? 16 : (m % 8 == 0) ? 8 : 4;
     if (s.dim == 3) {
@@ -589,7 +593,9 @@ int g_march_fused = 1;  // ekcg_tune key 9
 int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, int m,
                          double* partials, unsigned int* counter, double* S, EkcgCtrl* ctrl, int iteration, double tol,
                          int finalize, int max_ctas, cudaStream_t st) {
-    if (!g_march_fused || m != 16 || ldx != 16 || (reinterpret_cast<uintptr_t>(X) & 15)) return EKCG_EINVAL;
+    if (!g_march_fused || m != 16 || ldx != 16 || (reinterpret_cast<uintptr_t>(X) & 15) ||
+        (s.row_end - s.row_begin) * 16 < g_march_min_work)
+        return EKCG_EINVAL;
     FusedArgs fa{};
     fa.partials = partials;
     fa.counter = counter;
@@ -607,7 +613,7 @@ int launch_march_xr(const EkcgStencil& s, const UniformFaces& uf, const double* 
                     int k, int kmax, int stag, double* history, int do_finish, double* rho2_out, int max_ctas,
                     cudaStream_t st) {
     if (!g_march_fused || m != 16 || ldx != 16 || ldy % 2 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) ||
-        (reinterpret_cast<uintptr_t>(Y) & 15))
+        (reinterpret_cast<uintptr_t>(Y) & 15) || (s.row_end - s.row_begin) * 16 < g_march_min_work)
         return EKCG_EINVAL;
     FusedArgs fa{};
     fa.partials = partials;

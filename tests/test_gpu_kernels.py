@@ -94,6 +94,7 @@ def test_stencil_march_kernel(shape, kappa, m):
     ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, X)
     Xd = dev(X)
     outs = []
+    assert _lib.query("ekcg_tune", 12, 0) == 0  # march kernel at any size
     try:
         for march in (1, 0):
             assert _lib.query("ekcg_tune", 3, march) == 0
@@ -113,6 +114,7 @@ def test_stencil_march_kernel(shape, kappa, m):
         part = Yd.cpu().numpy()
     finally:
         _lib.query("ekcg_tune", 3, 1)
+        _lib.query("ekcg_tune", 12, 1 << 21)
     assert np.array_equal(outs[0], ref)
     assert np.array_equal(outs[1], ref)
     assert np.array_equal(part[lo:hi], ref[lo:hi])

@@ -265,6 +265,27 @@ def test_fused_matches_unfused(floors_golden, idx, edge):
     assert hist_dev(a.residual_history, b.residual_history, k=10) <= (0.5 if chaotic else 1e-9)
 
 
+@pytest.mark.parametrize("idx,edge", [(2, 16), (2, 12), (4, 10)])
+def test_march_fused_kernels_match_row_kernels(idx, edge):
+    """Plane-marching stencil kernels (plain, fused A-CholQR, fused x/r update),
+    forced at small sizes (ekcg_tune key 12), against the row-parallel kernels."""
+    from paper_2305_19013_b200 import _lib
+    from paper_2305_19013_b200.engine import DeviceEngine
+    prob = make_config(idx, edge)
+    cfg = SolverConfig(**dict(prob.solver_kwargs, kmax=30))
+    op = prob.stencil()
+    reps = []
+    try:
+        for march in (0, 1):
+            assert _lib.query("ekcg_tune", 12, 0 if march else 1 << 62) == 0
+            reps.append(DeviceEngine(op, prob.partition, cfg).solve(prob.b)[1])
+    finally:
+        _lib.query("ekcg_tune", 12, 1 << 21)
+    a, b = reps
+    assert a.iterations == b.iterations
+    assert hist_dev(a.residual_history, b.residual_history) <= 1e-10
+
+
 @pytest.mark.parametrize("idx,edge,form", [(3, 16, "stencil"), (3, 16, "csr"), (1, 100, "stencil"),
                                            (5, 64, "stencil")])
 def test_lean_scheme_matches_cached(floors_golden, solves_golden, idx, edge, form):
