@@ -325,6 +325,60 @@ gram_generic_kernel(const double* const* __restrict__ Xs, int ldx, int m1, const
     }
 }
 
+// X_i^T y for a vector y (m2 = 1) and m1 = 4 LN columns, 16-B aligned rows:
+// LN lanes per row, 4 columns per lane, U row groups in flight per warp; the
+// CTA's warps are combined in fixed order into its partial (same layout as
+// the Gram kernels).
+template <int LN, int U>
+__global__ void __launch_bounds__(256)
+gemvt4_kernel(const double* const* __restrict__ Xs, int ldx, int d, const double* __restrict__ y, long long n,
+              long long rows_chunk, double* __restrict__ partials, const int* __restrict__ live) {
+    EKCG_GATE(live);
+    constexpr int M = 4 * LN, RPW = 32 / LN;
+    __shared__ double red[8][M];
+    const int i = blockIdx.y;
+    const double* __restrict__ X = Xs[i];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int sub = lane / LN, li = lane % LN;
+    const long long r0 = blockIdx.x * rows_chunk;
+    const long long r1 = min(n, r0 + rows_chunk);
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    for (long long base = r0 + (long long)warp * RPW * U; base < r1; base += 8LL * RPW * U) {
+        double2 a[U][2];
+        double yv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const long long r = base + u * RPW + sub;
+            const bool ok = r < r1;
+            const double2* row = reinterpret_cast<const double2*>(X + r * ldx) + 2 * li;
+            a[u][0] = ok ? __ldg(row) : make_double2(0.0, 0.0);
+            a[u][1] = ok ? __ldg(row + 1) : make_double2(0.0, 0.0);
+            yv[u] = ok ? __ldg(y + r) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            acc[0] += a[u][0].x * yv[u];
+            acc[1] += a[u][0].y * yv[u];
+            acc[2] += a[u][1].x * yv[u];
+            acc[3] += a[u][1].y * yv[u];
+        }
+    }
+#pragma unroll
+    for (int off = 16; off >= LN; off >>= 1)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[c] += __shfl_xor_sync(0xffffffffu, acc[c], off);
+    if (sub == 0)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) red[warp][4 * li + c] = acc[c];
+    __syncthreads();
+    if (threadIdx.x < M) {
+        double s = red[0][threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) s += red[w][threadIdx.x];
+        partials[((long long)blockIdx.x * d + i) * M + threadIdx.x] = s;
+    }
+}
+
 // out[j] = sum_p partials[p*len + j].  Block = W warps x 32 lanes; lane owns
 // output j = 32*blockIdx.x + lane, warp w sums p = w, w+W, ... (4 loads in
 // flight), then the W warp sums are combined in fixed order: deterministic.
@@ -836,7 +890,19 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     // DMMA variants with m >= 16 load 16-B fragments pairs: even leading
     // dimensions, 16-B aligned Y (and blocks, by contract); else generic.
     if (m1 >= 16 && ((ldx | ldy) % 2 != 0 || (reinterpret_cast<uintptr_t>(Y) & 15))) fn = nullptr;
-    if (fn != nullptr && launch_gram_stream(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, partials, live, st) == EKCG_OK) {
+    const bool vec4 = (m2 == 1) && (m1 % 4 == 0) && (m1 <= 128) && (ldx % 2 == 0) &&
+                      ((m1 / 4) & (m1 / 4 - 1)) == 0;  // LN = m1/4 a power of two
+    if (vec4) {
+        const dim3 g(chunks, d);
+        switch (m1) {
+            case 4: gemvt4_kernel<1, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 8: gemvt4_kernel<2, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 16: gemvt4_kernel<4, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 32: gemvt4_kernel<8, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 64: gemvt4_kernel<16, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+            default: gemvt4_kernel<32, 2><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+        }
+    } else if (fn != nullptr && launch_gram_stream(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, partials, live, st) == EKCG_OK) {
         // streamed (TMA bulk) Gram, stream.cu
     } else if (fn != nullptr) {
         fn<<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);

@@ -209,7 +209,7 @@ class ShardedEngine(DeviceEngine):
             self._gram(WB_arr, m, 1, m, self.WC.data_ptr(), m, m, self.G.data_ptr(), tag="gram_self")
         self.comm.allreduce_(self.G[: m * m])
         _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
-        if fused:
+        if fused_st:
             _lib.call("ekcg_update_vec", WB_arr, m, self.S.data_ptr(), lq(blk), m, m, n, self.r.data_ptr(),
                       part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st)
         else:
