@@ -39,6 +39,7 @@ int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const 
                          cudaStream_t st);
 extern int g_update_stream;
 extern int g_march_fused;
+extern int g_fused_variant;
 
 int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
@@ -839,6 +840,10 @@ extern "C" int ekcg_tune(int key, long long value) {
     }
     if (key == 3 && value >= 0 && value <= 1) {
         g_stencil_march = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 13 && value >= 0 && value <= 6) {
+        g_fused_variant = (int)value;
         return EKCG_OK;
     }
     if (key == 12 && value >= 0) {

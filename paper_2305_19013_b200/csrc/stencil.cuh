@@ -259,6 +259,7 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
 extern int g_stencil_march;  // ekcg_tune key 3
 extern int g_march_variant;  // ekcg_tune key 4
 extern int g_march_fused;    // ekcg_tune key 9
+extern int g_fused_variant;  // ekcg_tune key 13
 // below this many block entries (rows x columns) the row-parallel kernels win (ekcg_tune key 12)
 extern long long g_march_min_work;
 // Fused plane-marching kernels for m = 16 (stencil_march.cu); EKCG_EINVAL when they do not apply.

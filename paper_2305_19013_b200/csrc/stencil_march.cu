@@ -508,7 +508,7 @@ stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil
 
 template <class P, int EPI>
 int launch_march_fused(const EkcgStencil& s, const UniformFaces& uf, const double* X, int max_ctas,
-                       const FusedArgs& fa, cudaStream_t st) {
+                       const FusedArgs& fa, cudaStream_t st, int items_per_cta = 1, int min_planes = 4) {
     constexpr int DIM = P::DIM;
     const long long plane = (DIM == 3) ? (long long)s.nx * s.ny : (long long)s.nx;
     if (s.row_begin % plane != 0 || s.row_end % plane != 0) return EKCG_EINVAL;
@@ -536,10 +536,10 @@ int launch_march_fused(const EkcgStencil& s, const UniformFaces& uf, const doubl
     const long long tiles = (DIM == 3) ? (long long)((s.nx + P::TX - 1) / P::TX) * ((s.ny + P::TY - 1) / P::TY)
                                        : (long long)((s.nx + P::TX - 1) / P::TX);
     int grid = resident < max_ctas ? resident : max_ctas;
-    // plane chunks: about one work item per resident CTA, marches of >= 4 planes
+    // plane chunks: about items_per_cta work items per resident CTA, marches of >= min_planes planes
     const int planes = we - wb;
-    long long wchunks = (grid + tiles - 1) / tiles;
-    if (wchunks > planes / 4) wchunks = planes / 4;
+    long long wchunks = ((long long)grid * items_per_cta + tiles - 1) / tiles;
+    if (wchunks > planes / min_planes) wchunks = planes / min_planes;
     if (wchunks < 1) wchunks = 1;
     const int wchunk = (int)((planes + wchunks - 1) / wchunks);
     wchunks = (planes + wchunk - 1) / wchunk;
@@ -589,6 +589,7 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
 // Fused plane-marching kernels for m = 16 (EKCG_EINVAL when they do not apply:
 // the caller takes the row-parallel fused kernels).
 int g_march_fused = 1;  // ekcg_tune key 9
+int g_fused_variant = 0;  // ekcg_tune key 13
 
 int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, int m,
                          double* partials, unsigned int* counter, double* S, EkcgCtrl* ctrl, int iteration, double tol,
@@ -604,7 +605,17 @@ int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const dou
     fa.tol = tol;
     fa.finalize = finalize;
     fa.out = S;
-    if (s.dim == 3) return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
+    if (s.dim == 3) {
+        switch (g_fused_variant) {
+            case 1: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
+            case 2: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
+            case 3: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 3, 2);
+            case 4: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 2, 4);
+            case 5: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 6, 2);
+            case 6: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 4, 1);
+            default: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 3, 2);
+        }
+    }
     return launch_march_fused<March<2, 16, 64, 1, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
 }
 
@@ -630,6 +641,16 @@ int launch_march_xr(const EkcgStencil& s, const UniformFaces& uf, const double* 
     fa.history = history;
     fa.do_finish = do_finish;
     fa.rho2_out = rho2_out;
-    if (s.dim == 3) return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
+    if (s.dim == 3) {
+        switch (g_fused_variant) {
+            case 1: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_XR>(s, uf, X, max_ctas, fa, st);
+            case 2: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
+            case 3: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_XR>(s, uf, X, max_ctas, fa, st, 3, 2);
+            case 4: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_XR>(s, uf, X, max_ctas, fa, st, 2, 4);
+            case 5: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 6, 2);
+            case 6: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 4, 1);
+            default: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 3, 2);
+        }
+    }
     return launch_march_fused<March<2, 16, 64, 1, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
 }

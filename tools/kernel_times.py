@@ -104,7 +104,8 @@ def fused_times():
         G = torch.empty(m * m, dtype=torch.float64, device=dev)
         hist = torch.zeros(16, dtype=torch.float64, device=dev)
         rho2 = torch.zeros(1, dtype=torch.float64, device=dev)
-        _lib.call("ekcg_tune", 9, int(sys.argv[-1]) if sys.argv[-1] in ("0", "1") else 1)
+        _lib.call("ekcg_tune", 9, 1)
+        _lib.call("ekcg_tune", 13, int(sys.argv[-1]) if sys.argv[-1].isdigit() else 0)
         tg = timeit(lambda: _lib.call("ekcg_stencil_cholinv", op.desc_ref(), X.data_ptr(), m, m, part.data_ptr(),
                                       cnt.data_ptr(), G.data_ptr(), ctrl.data_ptr(), 1, 1e-14, 0, st))
         tx = timeit(lambda: _lib.call("ekcg_stencil_xr", op.desc_ref(), X.data_ptr(), m, Y.data_ptr(), m, m,
