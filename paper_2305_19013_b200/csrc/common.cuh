@@ -14,11 +14,38 @@ extern unsigned long long g_ekcg_launches;
 // finalize kernel clears it when the solve stops (converged / maxiter /
 // breakdown), so iterations enqueued ahead of the host's status check
 // retire as empty launches.  nullptr means "always run".
+// Programmatic dependent launch: a kernel launched with the PDL attribute may
+// start while its predecessor on the stream drains; griddepcontrol.wait
+// blocks until the predecessor's writes are visible (a no-op otherwise), and
+// launch_dependents lets the successor's CTAs be scheduled early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 #define EKCG_GATE(live)                         \
     do {                                        \
+        pdl_wait();                             \
         if ((live) != nullptr && *(live) == 0)  \
             return;                             \
     } while (0)
+
+extern int g_pdl;  // 0: plain launches, 1: PDL attribute (ekcg_tune key 14)
+
+// <<<>>> replacement that adds the PDL launch attribute when enabled.
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                   Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 

@@ -43,7 +43,9 @@ extern int g_fused_variant;
 
 int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
-long long g_march_min_work = 1LL << 21;  // smaller grids take the row-parallel stencil kernels
+long long g_march_min_work = 1LL << 21;
+int g_pdl = 1;  // programmatic dependent launch on (ekcg_tune key 14)
+__device__ int g_pdl_trigger_dev = 0;  // smaller grids take the row-parallel stencil kernels
 int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
 int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
 namespace {
@@ -819,6 +821,7 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int lds, double
 __global__ void sub_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
                            long long n, const int* __restrict__ live) {
     EKCG_GATE(live);
+    if (g_pdl_trigger_dev) pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         out[i] = a[i] - b[i];
@@ -840,6 +843,12 @@ extern "C" int ekcg_tune(int key, long long value) {
     }
     if (key == 3 && value >= 0 && value <= 1) {
         g_stencil_march = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 14 && value >= 0 && value <= 2) {
+        g_pdl = value ? 1 : 0;
+        const int trig = value == 2 ? 1 : 0;
+        cudaMemcpyToSymbol(g_pdl_trigger_dev, &trig, sizeof(int));
         return EKCG_OK;
     }
     if (key == 13 && value >= 0 && value <= 6) {
@@ -900,21 +909,21 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     if (vec4) {
         const dim3 g(chunks, d);
         switch (m1) {
-            case 4: gemvt4_kernel<1, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 8: gemvt4_kernel<2, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 16: gemvt4_kernel<4, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 32: gemvt4_kernel<8, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 64: gemvt4_kernel<16, 4><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
-            default: gemvt4_kernel<32, 2><<<g, 256, 0, st>>>(Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 4: launch_k(gemvt4_kernel<1, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 8: launch_k(gemvt4_kernel<2, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 16: launch_k(gemvt4_kernel<4, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 32: launch_k(gemvt4_kernel<8, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 64: launch_k(gemvt4_kernel<16, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            default: launch_k(gemvt4_kernel<32, 2>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
         }
     } else if (fn != nullptr && launch_gram_stream(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, partials, live, st) == EKCG_OK) {
         // streamed (TMA bulk) Gram, stream.cu
     } else if (fn != nullptr) {
-        fn<<<grid, kGramThreads, 0, st>>>(Xs, ldx, d, Y, ldy, n, rc, partials, live);
+        launch_k(fn, grid, kGramThreads, 0, st, Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else {
         const int O = m1 * m2;
         size_t smem = (O <= 256) ? sizeof(double) * 256 : 0;
-        gram_generic_kernel<<<dim3(chunks, d), 256, smem, st>>>(Xs, ldx, m1, Y, ldy, m2, n, rc, partials, live);
+        launch_k(gram_generic_kernel, dim3(chunks, d), 256, smem, st, Xs, ldx, m1, Y, ldy, m2, n, rc, partials, live);
     }
     ++g_ekcg_launches;
     return launch_status();
@@ -926,7 +935,7 @@ extern "C" int ekcg_reduce(const double* partials, int chunks, long long len, do
     int warps = chunks < 32 ? chunks : 32;
     long long blocks = (len + 31) / 32;
     // keep enough warps in flight when there are few outputs
-    reduce_kernel<<<(unsigned)blocks, 32 * warps, 0, as_stream(stream)>>>(partials, chunks, len, out, live);
+    launch_k(reduce_kernel, (unsigned)blocks, 32 * warps, 0, as_stream(stream), partials, chunks, len, out, live);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -948,10 +957,10 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
     if (launch_update_stream(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo, m2, beta, sign, n, live, st) == EKCG_OK) {
         // streamed (TMA bulk) update, stream.cu
     } else if (m1 == m2 && even && m1 == 8) {
-        (g_upd_il ? update_dmma_kernel<8, 4, true> : update_dmma_kernel<8, 4, false>)<<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        launch_k(g_upd_il ? update_dmma_kernel<8, 4, true> : update_dmma_kernel<8, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                   sign, n, live);
     } else if (m1 == m2 && even && m1 == 16) {
-        (g_upd_il ? update_dmma_kernel<16, 4, true> : update_dmma_kernel<16, 4, false>)<<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        launch_k(g_upd_il ? update_dmma_kernel<16, 4, true> : update_dmma_kernel<16, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
     } else if (m1 == m2 && even && (m1 == 32 || m1 == 64) && (size_t)d * m1 * (m1 + 4) * 8 <= 200 * 1024) {
         const size_t smem = (size_t)d * m1 * (m1 + 4) * sizeof(double);
@@ -961,20 +970,20 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
         if (m1 == 32) {
             auto fn = update_smem_kernel<32, 4>;
             cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            fn<<<grid, 256, smem, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
+            launch_k(fn, grid, 256, smem, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
         } else {
             auto fn = update_smem_kernel<64, 2>;
             cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            fn<<<grid, 256, smem, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
+            launch_k(fn, grid, 256, smem, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
         }
     } else if (m1 == m2 && even && m1 == 32) {
-        update_dmma_kernel<32, 4><<<grid_rows(32), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        launch_k(update_dmma_kernel<32, 4>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
     } else if (m1 == m2 && even && m1 == 64) {
-        update_dmma_kernel<64, 2><<<grid_rows(16), 128, 0, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        launch_k(update_dmma_kernel<64, 2>, grid_rows(16), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
     } else {
-        update_generic_kernel<<<grid_for(n * m2, 256), 256, 0, st>>>(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo,
+        launch_k(update_generic_kernel, grid_for(n * m2, 256), 256, 0, st, Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo,
                                                                      m2, beta, sign, n, live);
     }
     ++g_ekcg_launches;
@@ -989,8 +998,8 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
     if (m < 1 || m > 256 || ldw < m || ldaw < m || n < 1) return EKCG_EINVAL;
     cudaStream_t st = as_stream(stream);
     const int g = vec_chunks(n);
-#define XR_LAUNCH(L) xr_update_kernel<L><<<g, kVecThreads, 0, st>>>(W, ldw, AW, ldaw, alpha, m, x, r, n, rho2_partials, live)
-#define XR4_LAUNCH(LN) xr_update4_kernel<LN, 4><<<g, kVecThreads, 0, st>>>(W, ldw, AW, ldaw, alpha, x, r, n, rho2_partials, live)
+#define XR_LAUNCH(L) launch_k(xr_update_kernel<L>, g, kVecThreads, 0, st, W, ldw, AW, ldaw, alpha, m, x, r, n, rho2_partials, live)
+#define XR4_LAUNCH(LN) launch_k(xr_update4_kernel<LN, 4>, g, kVecThreads, 0, st, W, ldw, AW, ldaw, alpha, x, r, n, rho2_partials, live)
     const bool al = (ldw % 2 == 0) && (ldaw % 2 == 0) && ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(AW) |
                                                            reinterpret_cast<uintptr_t>(alpha)) % 16 == 0);
     if (al && m == 64) XR4_LAUNCH(16);
@@ -1011,7 +1020,7 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
 
 extern "C" int ekcg_sumsq(const double* v, long long n, double* partials, const int* live, void* stream) {
     if (n < 1) return EKCG_EINVAL;
-    sumsq_kernel<<<vec_chunks(n), kVecThreads, 0, as_stream(stream)>>>(v, n, partials, live);
+    launch_k(sumsq_kernel, vec_chunks(n), kVecThreads, 0, as_stream(stream), v, n, partials, live);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -1020,7 +1029,7 @@ extern "C" int ekcg_block_diag_apply(const double* data, const long long* offs, 
                                      const int* row_block, int transpose, const double* X, int ldx, double* Y,
                                      int ldy, long long n, int m, const int* live, void* stream) {
     if (n < 1 || m < 1 || ldx < m || ldy < m || X == Y) return EKCG_EINVAL;
-    block_diag_apply_kernel<<<grid_for(n * m, 256), 256, 0, as_stream(stream)>>>(data, offs, starts, row_block,
+    launch_k(block_diag_apply_kernel, grid_for(n * m, 256), 256, 0, as_stream(stream), data, offs, starts, row_block,
                                                                                  transpose, X, ldx, Y, ldy, n, m,
                                                                                  live);
     ++g_ekcg_launches;
@@ -1031,7 +1040,7 @@ extern "C" int ekcg_block_trsv(const double* L, const long long* offs, const int
                                int transpose, const double* X, int ldx, double* Y, int ldy, int m,
                                const int* live, void* stream) {
     if (nblocks < 1 || m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
-    block_trsv_kernel<<<grid_for((long long)nblocks * m, 128), 128, 0, as_stream(stream)>>>(
+    launch_k(block_trsv_kernel, grid_for((long long)nblocks * m, 128), 128, 0, as_stream(stream), 
         L, offs, starts, nblocks, transpose, X, ldx, Y, ldy, m, live);
     ++g_ekcg_launches;
     return launch_status();
@@ -1041,7 +1050,7 @@ extern "C" int ekcg_copy_cols(const double* src, int lds, double* dst, int ldd, 
                               const int* live, void* stream) {
     if (n < 0 || w < 1 || lds < w || ldd < w) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
-    copy_cols_kernel<<<grid_for(n * w, 256), 256, 0, as_stream(stream)>>>(src, lds, dst, ldd, n, w, live);
+    launch_k(copy_cols_kernel, grid_for(n * w, 256), 256, 0, as_stream(stream), src, lds, dst, ldd, n, w, live);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -1049,7 +1058,7 @@ extern "C" int ekcg_copy_cols(const double* src, int lds, double* dst, int ldd, 
 extern "C" int ekcg_sub(const double* a, const double* b, double* out, long long n, const int* live,
                         void* stream) {
     if (n < 1) return EKCG_EINVAL;
-    sub_kernel<<<grid_for(n, 256), 256, 0, as_stream(stream)>>>(a, b, out, n, live);
+    launch_k(sub_kernel, grid_for(n, 256), 256, 0, as_stream(stream), a, b, out, n, live);
     ++g_ekcg_launches;
     return launch_status();
 }

@@ -59,6 +59,7 @@ update_epi_kernel(const double* const* __restrict__ Qs, int ldq, int d, const do
                   const double* Win, int ldwi, double* Wout, int ldwo, double beta, double sign, long long n,
                   const double* __restrict__ vec, double* __restrict__ partials, unsigned int* counter,
                   double* out, EkcgCtrl* ctrl, int iteration, double tol) {
+    pdl_wait();
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
     constexpr int NT = M / 8;
@@ -203,6 +204,7 @@ __global__ void __launch_bounds__(256)
 stencil_cholinv_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X, int ldx,
                        double* __restrict__ partials, unsigned int* counter, double* Sout, EkcgCtrl* ctrl,
                        int iteration, double tol, int finalize) {
+    pdl_wait();
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
     constexpr int G = M / VEC;
@@ -294,6 +296,7 @@ stencil_xr_kernel(EkcgStencil s, UniformFaces uf, const double* __restrict__ X, 
                   int ldy, int m, const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ r,
                   double* __restrict__ partials, unsigned int* counter, EkcgCtrl* ctrl, int k, int kmax,
                   int stagnation_window, double* __restrict__ history, int do_finish, double* rho2_out) {
+    pdl_wait();
     if (ctrl->live == 0) return;
     __shared__ double sa[64];
     __shared__ double wsum[8];
@@ -390,7 +393,7 @@ int launch_update_epi(const double* const* Qs, int ldq, int d, const double* C, 
     if (!set_smem((const void*)fn, smem)) return EKCG_ELAUNCH;
     long long tiles = (n + RT - 1) / RT;
     int grid = (int)(tiles < kFusedCtas ? tiles : kFusedCtas);
-    fn<<<grid, 128, smem, st>>>(Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, vec, partials, counter, out,
+    launch_k(fn, grid, 128, smem, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, vec, partials, counter, out,
                                 ctrl, iteration, tol);
     return EKCG_OK;
 }
@@ -412,7 +415,7 @@ int launch_stencil_cholinv(const EkcgStencil& s, const UniformFaces& uf, long lo
     if (!set_smem((const void*)fn, smem)) return EKCG_ELAUNCH;
     long long blocks = (n + R - 1) / R;
     int grid = (int)(blocks < kFusedCtas ? blocks : kFusedCtas);
-    fn<<<grid, dim3(G, R), smem, st>>>(s, uf, X, ldx, partials, counter, Sout, ctrl, iteration, tol, finalize);
+    launch_k(fn, grid, dim3(G, R), smem, st, s, uf, X, ldx, partials, counter, Sout, ctrl, iteration, tol, finalize);
     return EKCG_OK;
 }
 
@@ -525,13 +528,13 @@ extern "C" int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx
     long long blocks = (n + block.y - 1) / block.y;
     int grid = (int)(blocks < kFusedCtas ? blocks : kFusedCtas);
     if (vec == 4)
-        stencil_xr_kernel<4><<<grid, block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k,
+        launch_k(stencil_xr_kernel<4>, grid, block, 0, st, s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k,
                                                     kmax, stagnation_window, history, do_finish, rho2_out);
     else if (vec == 2)
-        stencil_xr_kernel<2><<<grid, block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k,
+        launch_k(stencil_xr_kernel<2>, grid, block, 0, st, s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k,
                                                     kmax, stagnation_window, history, do_finish, rho2_out);
     else
-        stencil_xr_kernel<1><<<grid, block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k,
+        launch_k(stencil_xr_kernel<1>, grid, block, 0, st, s, uf, X, ldx, Y, ldy, m, alpha, x, r, partials, counter, c, k,
                                                     kmax, stagnation_window, history, do_finish, rho2_out);
     ++g_ekcg_launches;
     return launch_status();

@@ -22,6 +22,7 @@ constexpr int kSmallThreads = 256;
 __global__ void __launch_bounds__(kSmallThreads)
 prechol_kernel(const double* __restrict__ Graw, int m, double* __restrict__ S0, EkcgCtrl* ctrl,
                int iteration, double tol) {
+    pdl_wait();
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
     double* G = sm;
@@ -33,6 +34,7 @@ prechol_kernel(const double* __restrict__ Graw, int m, double* __restrict__ S0, 
 __global__ void __launch_bounds__(kSmallThreads)
 cholinv_kernel(const double* __restrict__ Gin, int m, double* __restrict__ Sout, EkcgCtrl* ctrl, int iteration,
                double tol) {
+    pdl_wait();
     if (ctrl->live == 0) return;
     extern __shared__ double sm[];
     double* G = sm;
@@ -44,6 +46,7 @@ cholinv_kernel(const double* __restrict__ Gin, int m, double* __restrict__ Sout,
 __global__ void __launch_bounds__(kSmallThreads)
 cholesky_kernel(const double* __restrict__ Bin, int m, double tol, double* __restrict__ Rout,
                 double* __restrict__ info) {
+    pdl_wait();
     extern __shared__ double sm[];
     double* B = sm;
     double* R = B + m * m;
@@ -62,6 +65,7 @@ cholesky_kernel(const double* __restrict__ Bin, int m, double tol, double* __res
 
 __global__ void start_kernel(EkcgCtrl* ctrl, const double* __restrict__ rho2, double tol,
                              double* __restrict__ history) {
+    pdl_wait();
     double rho0 = sqrt(*rho2);
     history[0] = rho0;
     ctrl->rho0 = rho0;
@@ -87,6 +91,7 @@ __global__ void start_kernel(EkcgCtrl* ctrl, const double* __restrict__ rho2, do
 // solvers.py:398-415 (history append, stagnation guard) and :357 (loop test).
 __global__ void finish_kernel(EkcgCtrl* ctrl, const double* __restrict__ rho2, int k, int kmax,
                               int stagnation_window, double* __restrict__ history) {
+    pdl_wait();
     if (ctrl->live == 0) return;
     finish_body(ctrl, *rho2, k, kmax, stagnation_window, history);
 }
@@ -108,7 +113,7 @@ extern "C" int ekcg_prechol(const double* Graw, int m, double* S0, void* ctrl, i
     if (m < 1 || m > kMaxM || ctrl == nullptr) return EKCG_EINVAL;
     size_t smem = 3 * sizeof(double) * m * m;
     if (!set_smem((const void*)prechol_kernel, smem)) return EKCG_ELAUNCH;
-    prechol_kernel<<<1, kSmallThreads, smem, as_stream(stream)>>>(Graw, m, S0, (EkcgCtrl*)ctrl, iteration, tol);
+    launch_k(prechol_kernel, 1, kSmallThreads, smem, as_stream(stream), Graw, m, S0, (EkcgCtrl*)ctrl, iteration, tol);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -118,7 +123,7 @@ extern "C" int ekcg_cholinv(const double* G, int m, double* S, void* ctrl, int i
     if (m < 1 || m > kMaxM || ctrl == nullptr) return EKCG_EINVAL;
     size_t smem = 3 * sizeof(double) * m * m;
     if (!set_smem((const void*)cholinv_kernel, smem)) return EKCG_ELAUNCH;
-    cholinv_kernel<<<1, kSmallThreads, smem, as_stream(stream)>>>(G, m, S, (EkcgCtrl*)ctrl, iteration, tol);
+    launch_k(cholinv_kernel, 1, kSmallThreads, smem, as_stream(stream), G, m, S, (EkcgCtrl*)ctrl, iteration, tol);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -127,7 +132,7 @@ extern "C" int ekcg_cholesky(const double* B, int m, double tol, double* R, doub
     if (m < 1 || m > kMaxM) return EKCG_EINVAL;
     size_t smem = 2 * sizeof(double) * m * m;
     if (!set_smem((const void*)cholesky_kernel, smem)) return EKCG_ELAUNCH;
-    cholesky_kernel<<<1, kSmallThreads, smem, as_stream(stream)>>>(B, m, tol, R, info);
+    launch_k(cholesky_kernel, 1, kSmallThreads, smem, as_stream(stream), B, m, tol, R, info);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -136,7 +141,7 @@ extern "C" int ekcg_ctrl_bytes(void) { return (int)sizeof(EkcgCtrl); }
 
 extern "C" int ekcg_start(void* ctrl, const double* rho2, double tol, double* history, void* stream) {
     if (ctrl == nullptr || rho2 == nullptr || history == nullptr) return EKCG_EINVAL;
-    start_kernel<<<1, 1, 0, as_stream(stream)>>>((EkcgCtrl*)ctrl, rho2, tol, history);
+    launch_k(start_kernel, 1, 1, 0, as_stream(stream), (EkcgCtrl*)ctrl, rho2, tol, history);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -144,14 +149,14 @@ extern "C" int ekcg_start(void* ctrl, const double* rho2, double tol, double* hi
 extern "C" int ekcg_finish(void* ctrl, const double* rho2, int k, int kmax, int stagnation_window,
                            double* history, void* stream) {
     if (ctrl == nullptr) return EKCG_EINVAL;
-    finish_kernel<<<1, 1, 0, as_stream(stream)>>>((EkcgCtrl*)ctrl, rho2, k, kmax, stagnation_window, history);
+    launch_k(finish_kernel, 1, 1, 0, as_stream(stream), (EkcgCtrl*)ctrl, rho2, k, kmax, stagnation_window, history);
     ++g_ekcg_launches;
     return launch_status();
 }
 
 extern "C" int ekcg_store_norm(const double* rho2, double* checks, int slot, const int* live, void* stream) {
     if (slot < 0) return EKCG_EINVAL;
-    store_norm_kernel<<<1, 1, 0, as_stream(stream)>>>(rho2, checks, slot, live);
+    launch_k(store_norm_kernel, 1, 1, 0, as_stream(stream), rho2, checks, slot, live);
     ++g_ekcg_launches;
     return launch_status();
 }

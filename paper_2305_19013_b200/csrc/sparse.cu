@@ -190,7 +190,7 @@ extern "C" int ekcg_split(const double* v, const int* owner, double* W, long lon
     if (n < 0 || t < 1 || ldw < t) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
     RowLaunch L = row_launch(n, t < 32 ? t : 32);
-    split_kernel<<<L.grid, L.block, 0, as_stream(stream)>>>(v, owner, W, n, t, ldw, live);
+    launch_k(split_kernel, L.grid, L.block, 0, as_stream(stream), v, owner, W, n, t, ldw, live);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -201,7 +201,7 @@ extern "C" int ekcg_split_axpy(const double* v, const int* owner, const double* 
     if (n < 0 || t < 1 || ldw < t || ldp < t) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
     RowLaunch L = row_launch(n, t < 32 ? t : 32);
-    split_axpy_kernel<<<L.grid, L.block, 0, as_stream(stream)>>>(v, owner, Wprev, ldp, beta, beta_sign, W, n, t,
+    launch_k(split_axpy_kernel, L.grid, L.block, 0, as_stream(stream), v, owner, Wprev, ldp, beta, beta_sign, W, n, t,
                                                                  ldw, live);
     ++g_ekcg_launches;
     return launch_status();
@@ -212,7 +212,7 @@ extern "C" int ekcg_axpy_cols(double* W, int ldw, const double* Wprev, int ldp, 
     if (n < 0 || t < 1 || ldw < t || ldp < t) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
     RowLaunch L = row_launch(n, t < 32 ? t : 32);
-    axpy_cols_kernel<<<L.grid, L.block, 0, as_stream(stream)>>>(W, ldw, Wprev, ldp, beta, beta_sign, n, t, live);
+    launch_k(axpy_cols_kernel, L.grid, L.block, 0, as_stream(stream), W, ldw, Wprev, ldp, beta, beta_sign, n, t, live);
     ++g_ekcg_launches;
     return launch_status();
 }
@@ -223,7 +223,7 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
     if (n < 0 || m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
     RowLaunch L = row_launch(n, m < 64 ? m : 64);
-    csr_spmm_kernel<<<L.grid, L.block, 0, as_stream(stream)>>>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, m,
+    launch_k(csr_spmm_kernel, L.grid, L.block, 0, as_stream(stream), row_ptr, col_idx, values, X, ldx, Y, ldy, n, m,
                                                                live);
     ++g_ekcg_launches;
     return launch_status();
@@ -247,13 +247,13 @@ extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int l
     }
     if (aligned && m % 4 == 0) {
         RowLaunch L = row_launch(n, m / 4);
-        stencil_spmm_kernel<4><<<L.grid, L.block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, live);
+        launch_k(stencil_spmm_kernel<4>, L.grid, L.block, 0, st, s, uf, X, ldx, Y, ldy, m, live);
     } else if (aligned && m % 2 == 0) {
         RowLaunch L = row_launch(n, m / 2);
-        stencil_spmm_kernel<2><<<L.grid, L.block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, live);
+        launch_k(stencil_spmm_kernel<2>, L.grid, L.block, 0, st, s, uf, X, ldx, Y, ldy, m, live);
     } else {
         RowLaunch L = row_launch(n, m);
-        stencil_spmm_kernel<1><<<L.grid, L.block, 0, st>>>(s, uf, X, ldx, Y, ldy, m, live);
+        launch_k(stencil_spmm_kernel<1>, L.grid, L.block, 0, st, s, uf, X, ldx, Y, ldy, m, live);
     }
     ++g_ekcg_launches;
     return launch_status();

@@ -289,7 +289,7 @@ int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, 
     if (wchunks < 1) wchunks = 1;
     const int wchunk = (int)((planes + wchunks - 1) / wchunks);
     dim3 grid((unsigned)tiles, colchunks, (planes + wchunk - 1) / wchunk);
-    stencil_march_kernel<P><<<grid, P::NT, P::SMEM, st>>>(map, s, uf, Y, ldy, m, wb, we, wchunk, live);
+    launch_k(stencil_march_kernel<P>, grid, P::NT, P::SMEM, st, map, s, uf, Y, ldy, m, wb, we, wchunk, live);
     return EKCG_OK;
 }
 
@@ -329,6 +329,7 @@ template <class P, int EPI>
 __global__ void __launch_bounds__(P::NT, 2)
 stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil s, UniformFaces uf, int w_begin,
                            int w_end, int wchunk, int items, FusedArgs fa) {
+    pdl_wait();
     if (fa.ctrl->live == 0) return;
     constexpr int DIM = P::DIM, KC = P::KC, kNS = P::NS, kAhead = P::AHEAD, NODES = P::TX * P::TY;
     static_assert(KC == 16 && P::IPT == 1 && P::NT == 256 && NODES == 64, "16 columns, 64-node tiles");
@@ -545,7 +546,7 @@ int launch_march_fused(const EkcgStencil& s, const UniformFaces& uf, const doubl
     wchunks = (planes + wchunk - 1) / wchunk;
     const long long items = tiles * wchunks;
     if (items < grid) grid = (int)items;
-    stencil_march_fused_kernel<P, EPI><<<grid, P::NT, smem, st>>>(map, s, uf, wb, we, wchunk, (int)items, fa);
+    launch_k(stencil_march_fused_kernel<P, EPI>, grid, P::NT, smem, st, map, s, uf, wb, we, wchunk, (int)items, fa);
     return EKCG_OK;
 }
 

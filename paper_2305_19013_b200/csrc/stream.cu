@@ -145,7 +145,7 @@ int launch_gram16_stream(const double* const* Xs, int d, const double* Y, long l
         attr = true;
     }
     dim3 grid(chunks, (d + GB - 1) / GB);
-    fn<<<grid, 160, P::SMEM, st>>>(Xs, d, Y, n, rows_chunk, partials, live);
+    launch_k(fn, grid, 160, P::SMEM, st, Xs, d, Y, n, rows_chunk, partials, live);
     return EKCG_OK;
 }
 
@@ -282,7 +282,7 @@ int launch_update16_stream(const double* const* Qs, int d, const double* C, cons
     }
     const long long slabs = (n + R - 1) / R;
     const int g = (int)(slabs < grid ? slabs : grid);
-    fn<<<g, 160, smem, st>>>(Qs, d, C, Win, Wout, beta, sign, n, live);
+    launch_k(fn, g, 160, smem, st, Qs, d, C, Win, Wout, beta, sign, n, live);
     return EKCG_OK;
 }
 

@@ -17,6 +17,10 @@ prob = make_config(idx)
 cfg = pk.SolverConfig(**prob.solver_kwargs)
 op = prob.stencil()
 b = torch.as_tensor(prob.b, device="cuda")
+import os
+from paper_2305_19013_b200 import _lib  # noqa: E402
+if os.environ.get("PDL") is not None:
+    _lib.call("ekcg_tune", 14, int(os.environ["PDL"]))
 orig = DeviceEngine._enqueue_iteration
 for rep in range(3):
     evs, host = [], []
