@@ -21,9 +21,14 @@ extern unsigned long long g_ekcg_launches;
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+#ifndef EKCG_PDL_TRIGGER
+#define EKCG_PDL_TRIGGER 0  // early launch_dependents measured 1 % slower (tools/ab_lib.py)
+#endif
+
 #define EKCG_GATE(live)                         \
     do {                                        \
         pdl_wait();                             \
+        if (EKCG_PDL_TRIGGER) pdl_trigger();    \
         if ((live) != nullptr && *(live) == 0)  \
             return;                             \
     } while (0)

@@ -45,7 +45,6 @@ int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
 long long g_march_min_work = 1LL << 21;
 int g_pdl = 1;  // programmatic dependent launch on (ekcg_tune key 14)
-__device__ int g_pdl_trigger_dev = 0;  // smaller grids take the row-parallel stencil kernels
 int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
 int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
 namespace {
@@ -821,7 +820,6 @@ __global__ void copy_cols_kernel(const double* __restrict__ src, int lds, double
 __global__ void sub_kernel(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ out,
                            long long n, const int* __restrict__ live) {
     EKCG_GATE(live);
-    if (g_pdl_trigger_dev) pdl_trigger();
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x)
         out[i] = a[i] - b[i];
@@ -845,10 +843,8 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_stencil_march = (int)value;
         return EKCG_OK;
     }
-    if (key == 14 && value >= 0 && value <= 2) {
-        g_pdl = value ? 1 : 0;
-        const int trig = value == 2 ? 1 : 0;
-        cudaMemcpyToSymbol(g_pdl_trigger_dev, &trig, sizeof(int));
+    if (key == 14 && value >= 0 && value <= 1) {
+        g_pdl = (int)value;
         return EKCG_OK;
     }
     if (key == 13 && value >= 0 && value <= 6) {
