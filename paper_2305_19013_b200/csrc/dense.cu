@@ -38,6 +38,14 @@ int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const 
                          double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                          cudaStream_t st);
 extern int g_update_stream;
+extern int g_wide_stream;
+extern int g_wide_upd_variant;
+int gram_wide_slots(int gb);
+int launch_gram_wide(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
+                     int chunks, long long rows_chunk, int gb, double* partials, const int* live, cudaStream_t st);
+int launch_update_wide_any(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
+                           double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
+                           cudaStream_t st);
 extern int g_march_fused;
 extern int g_fused_variant;
 
@@ -254,19 +262,21 @@ int gram_chunks(long long n, int d, int m1, int m2) {
     int gb;
     GramFn fn = select_gram(d, m1, m2, gb);
     const long long groups = (d + gb - 1) / gb;
-    if (m1 == 16 && m2 == 16 && g_gram_stream && g_gram_target <= 0) {
-        // streamed Gram: one CTA per SM with long row ranges.  Pick the chunk
+    const bool wide = m1 == 32 && m2 == 32 && g_wide_stream && g_gram_target <= 0;
+    if ((m1 == 16 && m2 == 16 && g_gram_stream && g_gram_target <= 0) || wide) {
+        // streamed Gram: resident CTAs with long row ranges.  Pick the chunk
         // count whose CTA total fills its last wave best (equal work per CTA),
         // preferring fewer chunks; at least 1024 rows per chunk.
+        const long long slots = wide ? gram_wide_slots(gb) : 148;
         long long pmax = (n + 1023) / 1024;
-        const long long cap = (4 * 148 + groups - 1) / groups;
+        const long long cap = (4 * slots + groups - 1) / groups;
         if (pmax > cap) pmax = cap;
         if (pmax < 1) pmax = 1;
         long long best = 1;
         double best_eff = 0.0;
         for (long long p = 1; p <= pmax; ++p) {
             const long long ctas = p * groups;
-            const double eff = (double)ctas / (148.0 * (double)((ctas + 147) / 148));
+            const double eff = (double)ctas / ((double)slots * (double)((ctas + slots - 1) / slots));
             if (eff > best_eff + 0.01) {
                 best_eff = eff;
                 best = p;
@@ -843,6 +853,14 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_stencil_march = (int)value;
         return EKCG_OK;
     }
+    if (key == 16 && value >= 0 && value <= 2) {
+        g_wide_upd_variant = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 15 && value >= 0 && value <= 1) {
+        g_wide_stream = (int)value;
+        return EKCG_OK;
+    }
     if (key == 14 && value >= 0 && value <= 1) {
         g_pdl = (int)value;
         return EKCG_OK;
@@ -912,6 +930,8 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
             case 64: launch_k(gemvt4_kernel<16, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
             default: launch_k(gemvt4_kernel<32, 2>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
         }
+    } else if (fn != nullptr && launch_gram_wide(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, gb, partials, live, st) == EKCG_OK) {
+        // streamed (TMA bulk) Gram for 32-column blocks, stream_wide.cu
     } else if (fn != nullptr && launch_gram_stream(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, partials, live, st) == EKCG_OK) {
         // streamed (TMA bulk) Gram, stream.cu
     } else if (fn != nullptr) {
@@ -952,6 +972,8 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
     };
     if (launch_update_stream(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo, m2, beta, sign, n, live, st) == EKCG_OK) {
         // streamed (TMA bulk) update, stream.cu
+    } else if (launch_update_wide_any(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo, m2, beta, sign, n, live, st) == EKCG_OK) {
+        // streamed update for 32 / 64-column blocks, stream_wide.cu
     } else if (m1 == m2 && even && m1 == 8) {
         launch_k(g_upd_il ? update_dmma_kernel<8, 4, true> : update_dmma_kernel<8, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                   sign, n, live);

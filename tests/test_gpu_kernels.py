@@ -190,6 +190,42 @@ def test_block_update(m1, m2, n, beta):
         assert torch.equal(W2, Wout)
 
 
+@pytest.mark.parametrize("m", [32, 64])
+@pytest.mark.parametrize("d", [1, 2, 5, 7])
+@pytest.mark.parametrize("n", [63, 70_001])
+def test_wide_streamed_update_and_gram(m, d, n):
+    """Streamed m = 32 / 64 kernels (stream_wide.cu) against the register-direct ones
+    and torch: every depth (C_i resident in smem or not), ragged last slab, in place."""
+    rng = np.random.default_rng(m * 100 + d + n)
+    Qs = [dev(rng.standard_normal((n, m))) for _ in range(d)]
+    C = dev(rng.standard_normal((d * m, m)))
+    Win = dev(rng.standard_normal((n, m)))
+    tab = torch.tensor([q.data_ptr() for q in Qs], dtype=torch.int64, device=DEV)
+    outs = []
+    for wide, variant in ((1, 0), (1, 1), (1, 2), (0, 0)):
+        _lib.call("ekcg_tune", 15, wide)
+        _lib.call("ekcg_tune", 16, variant)
+        W = Win.clone()
+        _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m, W.data_ptr(),
+                  m, m, 1.0, -1.0, n, None, stream())
+        chunks = _lib.query("ekcg_gram_chunks", n, d, m, m)
+        part = torch.empty(chunks * d * m * m, dtype=torch.float64, device=DEV)
+        G = torch.empty(d * m * m, dtype=torch.float64, device=DEV)
+        _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Win.data_ptr(), m, m, n, part.data_ptr(), None, stream())
+        _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m * m, G.data_ptr(), None, stream())
+        outs.append((W, G.view(d, m, m)))
+    _lib.call("ekcg_tune", 15, 1)
+    _lib.call("ekcg_tune", 16, 0)
+    ref = Win - sum(Qs[i] @ C[i * m:(i + 1) * m] for i in range(d))
+    scale = sum((Qs[i].abs() @ C[i * m:(i + 1) * m].abs()) for i in range(d)).max().item() + 1.0
+    for W, G in outs:
+        assert (W - ref).abs().max().item() <= 1e-13 * scale
+        for i in range(d):
+            gref = Qs[i].T @ Win
+            gscale = (Qs[i].abs().T @ Win.abs()).max().item() + 1e-300
+            assert (G[i] - gref).abs().max().item() <= 1e-13 * gscale
+
+
 @pytest.mark.parametrize("m", [1, 2, 6, 16, 64])
 def test_cholesky_and_trsm(m):
     rng = np.random.default_rng(m)

@@ -41,23 +41,30 @@ def sweep(m, shape, d):
     chunks = _lib.query("ekcg_gram_chunks", n, d, m, m)
     part = torch.empty(max(2048 * d * m * m, 1 << 20), dtype=torch.float64, device=dev)
     C = torch.randn(d * m * m, dtype=torch.float64, device=dev) * 0.01
-    for gs in ((0, 3) if m == 16 else (0,)):
+    for gs in ((0, 3) if m == 16 else (0, 1)):
         for tgt in (0,):
-            _lib.call("ekcg_tune", 7, gs)
+            _lib.call("ekcg_tune", 7 if m == 16 else 15, gs)
             _lib.call("ekcg_tune", 2, tgt)
             ch = _lib.query("ekcg_gram_chunks", n, d, m, m)
+            part = torch.empty(max(ch * d * m * m, 1 << 20), dtype=torch.float64, device=dev)
             g = timeit(lambda: _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Y.data_ptr(), m, m, n, part.data_ptr(),
                                          None, st))
             out[f"gram_s{gs}_t{tgt}"] = dict(s=g, GBs=8 * (d + 1) * n * m / g / 1e9, TF=2 * d * m * m * n / g / 1e12)
     _lib.call("ekcg_tune", 7, 3)
     _lib.call("ekcg_tune", 2, 0)
     _lib.call("ekcg_tune", 5, -1)
-    for us in ((0, 2, 5, 6, 7) if m == 16 else (0,)):
-        _lib.call("ekcg_tune", 8, us)
+    for us in ((0, 2, 5, 6, 7) if m == 16 else (0, 10, 11, 12)):
+        if m == 16:
+            _lib.call("ekcg_tune", 8, us)
+        else:  # 0: register-direct kernels; 10 + v: streamed variant v
+            _lib.call("ekcg_tune", 15, 1 if us else 0)
+            _lib.call("ekcg_tune", 16, max(us - 10, 0))
         u = timeit(lambda: _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m,
                                      W.data_ptr(), m, m, 1.0, -1.0, n, None, st))
         out[f"update_s{us}"] = dict(s=u, GBs=8 * (d + 2) * n * m / u / 1e9, TF=2 * d * m * m * n / u / 1e12)
     _lib.call("ekcg_tune", 8, 2)
+    _lib.call("ekcg_tune", 15, 1)
+    _lib.call("ekcg_tune", 16, 0)
     op = StencilOperator(shape, 1.0)
     Z = torch.empty_like(Y)
     sp = timeit(lambda: op.apply(Y, m, Z, m, m))
@@ -69,9 +76,11 @@ def sweep(m, shape, d):
     return out
 
 
-if __name__ == "__main__" and "--fused" not in sys.argv and "--stencil" not in sys.argv:
-    cases = [(16, (64, 64, 64), 32), (16, (64, 64, 64), 110), (32, (128, 128, 128), 4), (64, (256, 256, 128), 3),
-             (64, (256, 256, 256), 2)]
+if __name__ == "__main__" and "--fused" not in sys.argv and "--stencil" not in sys.argv:  # [--wide]
+    cases = [(16, (64, 64, 64), 32), (16, (64, 64, 64), 110), (32, (128, 128, 128), 4), (32, (128, 128, 128), 1),
+             (64, (256, 256, 128), 3), (64, (256, 256, 256), 2), (64, (256, 256, 256), 1)]
+    if len(sys.argv) > 1 and sys.argv[1] == "--wide":
+        cases = [c for c in cases if c[0] >= 32]
     res = {}
     for m, shape, d in cases:
         key = f"m{m}_n{'x'.join(map(str, shape))}_d{d}"
