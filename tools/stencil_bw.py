@@ -17,6 +17,7 @@ from paper_2305_19013_b200.problems import make_config  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="2,3,4,5")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--variants", default="0", help="plane-march variants (ekcg_tune 4) to time")
 args = ap.parse_args()
 
 
@@ -42,8 +43,12 @@ for c in (int(v) for v in args.configs.split(",")):
     op = prob.stencil()
     widths = {2: [16], 3: [32, 16], 4: [16, 64], 5: [64]}[c]
     const = StencilOperator(op.shape, 1.0)
+    from paper_2305_19013_b200 import _lib
     for m in widths:
         if op.n * m * 16 > 100e9:
             continue
-        print(json.dumps({"config": c, "m": m, "field": op.field is not None, "op": bw(op, m, args.reps),
-                          "const_kappa": bw(const, m, args.reps)}), flush=True)
+        for v in (int(x) for x in args.variants.split(",")):
+            _lib.call("ekcg_tune", 4, v)
+            print(json.dumps({"config": c, "m": m, "variant": v, "field": op.field is not None,
+                              "op": bw(op, m, args.reps), "const_kappa": bw(const, m, args.reps)}), flush=True)
+        _lib.call("ekcg_tune", 4, 0)
