@@ -16,6 +16,8 @@
 // per row (one per column group) and R rows per block, grid-striding over
 // rows -- no 64-bit integer division in the index math.
 // ---------------------------------------------------------------------------
+int g_csr_vec = 1;  // ekcg_tune key 17: vectorized CSR SpMM (0: one thread per (row, column), 2: at most 2 columns per thread)
+
 struct RowLaunch {
     dim3 grid, block;
 };
@@ -147,6 +149,83 @@ __global__ void csr_spmm_kernel(const long long* __restrict__ rp, const int* __r
     }
 }
 
+// Vectorized CSR SpMM: G = m / VEC threads per row, VEC contiguous columns per
+// thread (16-B loads of X / stores of Y for VEC >= 2).  Rows with at most 8
+// entries (every stencil-like row) load all their (col, value) pairs and X
+// gathers up front, predicated, so up to 8 independent gathers per thread are
+// in flight; the sum is then formed in the reference association
+// p0 + (((p1 + p2) + p3) + ...).  Longer rows take numpy's pairwise tail per
+// column (tail_pairwise).  Bitwise equal to csr_spmm_kernel.
+template <int VEC>
+__device__ __forceinline__ void load_xvec(const double* __restrict__ X, long long off, double (&v)[VEC]) {
+    if (VEC == 1) {
+        v[0] = __ldg(X + off);
+    } else {
+#pragma unroll
+        for (int h = 0; h < VEC / 2; ++h) {
+            const double2 t = __ldg(reinterpret_cast<const double2*>(X + off) + h);
+            v[2 * h] = t.x;
+            v[2 * h + 1] = t.y;
+        }
+    }
+}
+
+template <int VEC>
+__global__ void __launch_bounds__(256, VEC == 4 ? 2 : 3)
+csr_spmm_vec_kernel(const long long* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vv,
+                    const double* __restrict__ X, int ldx, double* __restrict__ Y, int ldy, long long n,
+                    const int* __restrict__ live) {
+    EKCG_GATE(live);
+    const int c0 = threadIdx.x * VEC;
+    ROW_LOOP(i, n) {
+        const long long lo = __ldg(rp + i), hi = __ldg(rp + i + 1);
+        const long long cnt = hi - lo - 1;  // tail length after p0
+        double y[VEC];
+        if (hi <= lo) {
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) y[v] = 0.0;  // unreachable for validated SPD matrices
+        } else if (cnt < 8) {
+            int cq[8];
+            double aq[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                cq[q] = q <= cnt ? __ldg(ci + lo + q) : 0;
+                aq[q] = q <= cnt ? __ldg(vv + lo + q) : 0.0;
+            }
+            double xq[8][VEC];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (q <= cnt) load_xvec<VEC>(X, (long long)cq[q] * ldx + c0, xq[q]);
+            }
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                const double p0 = mul_rn(aq[0], xq[0][v]);
+                if (cnt == 0) {
+                    y[v] = p0;
+                } else {
+                    double acc = mul_rn(aq[1], xq[1][v]);
+#pragma unroll
+                    for (int q = 2; q < 8; ++q)
+                        if (q <= cnt) acc = add_rn(acc, mul_rn(aq[q], xq[q][v]));
+                    y[v] = add_rn(p0, acc);
+                }
+            }
+        } else {
+            const double a0 = __ldg(vv + lo);
+            const long long x0 = (long long)__ldg(ci + lo) * ldx;
+            for (int v = 0; v < VEC; ++v)
+                y[v] = add_rn(mul_rn(a0, __ldg(X + x0 + c0 + v)), tail_pairwise(ci, vv, lo + 1, cnt, X, ldx, c0 + v));
+        }
+        if (VEC == 1) {
+            Y[i * ldy + c0] = y[0];
+        } else {
+#pragma unroll
+            for (int h = 0; h < VEC / 2; ++h)
+                reinterpret_cast<double2*>(Y + i * ldy + c0)[h] = make_double2(y[2 * h], y[2 * h + 1]);
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Grid stencil: the operator `_diffusion_matrix(shape, kappa)` assembles
 // (generators.py:25-60), generalised with per-axis coefficients c_axis
@@ -222,9 +301,22 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
                              const int* live, void* stream) {
     if (n < 0 || m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
-    RowLaunch L = row_launch(n, m < 64 ? m : 64);
-    launch_k(csr_spmm_kernel, L.grid, L.block, 0, as_stream(stream), row_ptr, col_idx, values, X, ldx, Y, ldy, n, m,
-                                                               live);
+    cudaStream_t st = as_stream(stream);
+    const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0 &&
+                      ldx % 2 == 0 && ldy % 2 == 0;
+    if (g_csr_vec == 1 && m % 4 == 0 && m / 4 <= 256 && al16) {
+        RowLaunch L = row_launch(n, m / 4);
+        launch_k(csr_spmm_vec_kernel<4>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
+    } else if (g_csr_vec && m % 2 == 0 && m / 2 <= 256 && al16) {
+        RowLaunch L = row_launch(n, m / 2);
+        launch_k(csr_spmm_vec_kernel<2>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
+    } else if (g_csr_vec && m == 1) {
+        RowLaunch L = row_launch(n, 1);
+        launch_k(csr_spmm_vec_kernel<1>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
+    } else {
+        RowLaunch L = row_launch(n, m < 64 ? m : 64);
+        launch_k(csr_spmm_kernel, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, m, live);
+    }
     ++g_ekcg_launches;
     return launch_status();
 }

@@ -55,6 +55,34 @@ def test_csr_spmm_bitwise(kernels_golden, tag):
         assert np.array_equal(pk.spmm(A, X[:, :m].copy()), g[f"spmm_{tag}_Y"][:, :m])
 
 
+@pytest.mark.parametrize("m", [1, 2, 4, 6, 12, 32, 64])
+def test_csr_vectorized_equals_scalar_kernel(m):
+    """The vectorized CSR kernel (ekcg_tune 17) against the one-thread-per-(row, column)
+    kernel, bitwise, on rows of 1..20 entries (the < 8 fast path, the 8 / 9 boundary
+    and the pairwise tail)."""
+    rng = np.random.default_rng(m)
+    n = 5000
+    lens = rng.integers(1, 21, n)
+    lens[:25] = np.arange(1, 26) % 21 + 1
+    rp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(n, k, replace=False)) for k in lens]).astype(np.int32)
+    vals = rng.standard_normal(rp[-1])
+    X = dev(rng.standard_normal((n, m)))
+    rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
+    outs = []
+    for vec in (1, 2, 0):
+        _lib.call("ekcg_tune", 17, vec)
+        Y = torch.empty_like(X)
+        _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(), m, Y.data_ptr(),
+                  m, n, m, None, stream())
+        outs.append(Y.cpu().numpy())
+    _lib.call("ekcg_tune", 17, 1)
+    assert np.array_equal(outs[0].view(np.int64), outs[2].view(np.int64))
+    assert np.array_equal(outs[1].view(np.int64), outs[2].view(np.int64))
+    ref = orc.csr_spmm(rp, ci.astype(np.int64), vals, X.cpu().numpy())
+    assert np.array_equal(outs[0].view(np.int64), ref.view(np.int64))
+
+
 @pytest.mark.parametrize("idx,edge", [(1, 20), (2, 8), (3, 16), (4, 8), (5, 64)])
 @pytest.mark.parametrize("m", [1, 2, 7, 16, 32])
 def test_stencil_equals_csr_bitwise(idx, edge, m):

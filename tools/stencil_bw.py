@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--configs", default="2,3,4,5")
 ap.add_argument("--reps", type=int, default=10)
 ap.add_argument("--variants", default="0", help="plane-march variants (ekcg_tune 4) to time")
+ap.add_argument("--csr", action="store_true", help="also time the CSR SpMM of the same operator")
 args = ap.parse_args()
 
 
@@ -52,3 +53,15 @@ for c in (int(v) for v in args.configs.split(",")):
             print(json.dumps({"config": c, "m": m, "variant": v, "field": op.field is not None,
                               "op": bw(op, m, args.reps), "const_kappa": bw(const, m, args.reps)}), flush=True)
         _lib.call("ekcg_tune", 4, 0)
+        if args.csr:
+            from paper_2305_19013_b200.operators import CsrOperator
+            A = prob.csr()
+            cop = CsrOperator(A, "cuda")
+            for vec in (1, 2, 0):
+                _lib.call("ekcg_tune", 17, vec)
+                ms, _ = bw(cop, m, args.reps)
+                nbytes = 16.0 * op.n * m + 12.0 * A.nnz + 8.0 * (op.n + 1)
+                print(json.dumps({"config": c, "m": m, "csr_vec": vec, "csr_ms": ms,
+                                  "csr_GBs": round(nbytes / (ms / 1e3) / 1e9, 1)}), flush=True)
+            _lib.call("ekcg_tune", 17, 1)
+            del cop, A
