@@ -102,6 +102,14 @@ int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1, const dou
                       const double* Win, int ldwi, double* Wout, int ldwo, int m2,
                       double beta, double sign, long long n, const int* live, void* stream);
 
+/* out = W S for an upper-triangular m x m S (zeros below the diagonal): the
+ * Pre-CholQR / A-CholQR applies W R0^-1 and W0 R^-1 that replace
+ * trsm_right_inv (linalg.py:187-196, aortho.py:106,109).  Ws is a device
+ * array holding the one block pointer.  At m = 64 the blocks of S below the
+ * diagonal are skipped (FP64-bound width); other widths run ekcg_block_update. */
+int ekcg_tri_apply(const double* const* Ws, int ldw, const double* S, double* out, int ldo, int m,
+                   long long n, const int* live, void* stream);
+
 /* x += W alpha ; r -= AW alpha ; rho2_partials[p] = partial sum of r_new^2
  * (solvers.py:394-397).  Uses ekcg_vec_chunks(n) partials. */
 int ekcg_vec_chunks(long long n);

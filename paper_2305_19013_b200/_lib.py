@@ -29,6 +29,7 @@ SIGNATURES = {
     "ekcg_reduce": (c_int, [c_void_p, c_int, c_longlong, c_void_p, c_void_p, c_void_p]),
     "ekcg_block_update": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_int,
                                   c_int, c_double, c_double, c_longlong, c_void_p, c_void_p]),
+    "ekcg_tri_apply": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_int, c_int, c_longlong, c_void_p, c_void_p]),
     "ekcg_vec_chunks": (c_int, [c_longlong]),
     "ekcg_xr_update": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p, c_int, c_void_p, c_void_p,
                                c_longlong, c_void_p, c_void_p, c_void_p]),

@@ -54,6 +54,7 @@ int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
 long long g_march_min_work = 1LL << 21;
 int g_pdl = 1;  // programmatic dependent launch on (ekcg_tune key 14)
+int g_tri_skip = 1;  // ekcg_tune key 18: ekcg_tri_apply skips the zero blocks of S (m = 64)
 int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
 int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
 namespace {
@@ -533,7 +534,10 @@ update_dmma_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
 // CTA in shared memory (rows padded to M + 4 doubles so the 4 k-rows of a
 // fragment fall 8 banks apart) and B fragments come from smem; 8 warps per
 // CTA, each walking its own 8*MR-row tiles (no block barriers in the loop).
-template <int M, int MR>
+// TRI: d = 1 and C upper triangular (the Pre-CholQR / A-CholQR factor
+// S = R^-1, aortho.py:106,109): k-step pairs kp > nt multiply exact zeros and
+// are skipped (44 % of the DMMAs at M = 64); the products kept are the same.
+template <int M, int MR, bool TRI = false>
 __global__ void __launch_bounds__(256)
 update_smem_kernel(const double* const* __restrict__ Qs, int ldq, int d, const double* __restrict__ C,
                    const double* Win, int ldwi, double* Wout, int ldwo, double beta, double sign,
@@ -564,7 +568,7 @@ update_smem_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
         for (int i = 0; i < d; ++i) {
             const double* __restrict__ Q = Qs[i];
             const double* Ci = cs + i * M * LDC;
-#pragma unroll 2
+#pragma unroll (TRI ? KK / 2 : 2)
             for (int kp = 0; kp < KK / 2; ++kp) {
                 double2 afr[MR];
 #pragma unroll
@@ -576,17 +580,20 @@ update_smem_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
                 double bx[NT], by[NT];
 #pragma unroll
                 for (int nt = 0; nt < NT; ++nt) {
+                    if (TRI && kp > nt) continue;
                     bx[nt] = Ci[(8 * kp + 2 * lr) * LDC + 8 * nt + lc];
                     by[nt] = Ci[(8 * kp + 2 * lr + 1) * LDC + 8 * nt + lc];
                 }
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr].x, bx[nt]);
+                    for (int nt = 0; nt < NT; ++nt)
+                        if (!(TRI && kp > nt)) dmma_8x8x4(acc[mr][nt], afr[mr].x, bx[nt]);
 #pragma unroll
                 for (int mr = 0; mr < MR; ++mr)
 #pragma unroll
-                    for (int nt = 0; nt < NT; ++nt) dmma_8x8x4(acc[mr][nt], afr[mr].y, by[nt]);
+                    for (int nt = 0; nt < NT; ++nt)
+                        if (!(TRI && kp > nt)) dmma_8x8x4(acc[mr][nt], afr[mr].y, by[nt]);
             }
         }
         store_tile_rows<MR, NT>(acc, rbase, lc, lr, n, Win, ldwi, Wout, ldwo, beta, sign);
@@ -854,6 +861,10 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_stencil_march = (int)value;
         return EKCG_OK;
     }
+    if (key == 18 && value >= 0 && value <= 1) {
+        g_tri_skip = (int)value;
+        return EKCG_OK;
+    }
     if (key == 17 && value >= 0 && value <= 2) {
         g_csr_vec = (int)value;
         return EKCG_OK;
@@ -1011,6 +1022,25 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
     }
     ++g_ekcg_launches;
     return launch_status();
+}
+
+extern "C" int ekcg_tri_apply(const double* const* Ws, int ldw, const double* S, double* out, int ldo, int m,
+                              long long n, const int* live, void* stream) {
+    if (m < 1 || ldw < m || ldo < m || n < 0) return EKCG_EINVAL;
+    if (n == 0) return EKCG_OK;
+    const bool even = (ldw % 2 == 0) && (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (m == 64 && even && g_tri_skip) {
+        const size_t smem = (size_t)64 * (64 + 4) * sizeof(double);
+        long long tiles = (n + 15) / 16;
+        unsigned grid = grid_for(tiles, 8, 148LL * 8);
+        auto fn = update_smem_kernel<64, 2, true>;
+        cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        launch_k(fn, grid, 256, smem, as_stream(stream), Ws, ldw, 1, S, (const double*)nullptr, m, out, ldo, 0.0, 1.0,
+                 n, live);
+        ++g_ekcg_launches;
+        return launch_status();
+    }
+    return ekcg_block_update(Ws, ldw, 1, m, S, nullptr, m, out, ldo, m, 0.0, 1.0, n, live, stream);
 }
 
 extern "C" int ekcg_vec_chunks(long long n) { return vec_chunks(n); }

@@ -262,6 +262,11 @@ class DeviceEngine:
                                 m2, beta, sign, self.n, self.live, self.stream)
         self._timed(tag, run)
 
+    def _tri_apply(self, w_arr, ldw, s_ptr, out_ptr, ldo, m, tag="tri_apply"):
+        """out = W S with S upper triangular (W R^-1 of aortho.py:106,109)."""
+        self._timed(tag, lambda: _lib.call("ekcg_tri_apply", w_arr, ldw, s_ptr, out_ptr, ldo, m, self.n, self.live,
+                                           self.stream))
+
     def _apply_op(self, x_ptr, ldx, y_ptr, ldy, m, tag="spmm", live=-1):
         gate = self.live if live == -1 else live
         self._timed(tag, lambda: self.op.apply(x_ptr, ldx, y_ptr, ldy, m, gate, self.stream))
@@ -429,7 +434,7 @@ class DeviceEngine:
         if not have_s0:
             self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
             _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, self._karg(k), 1e-14, st)
-        self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WB, m, m, 0.0, 1.0, tag="tri_apply")
+        self._tri_apply(WA_arr, m, self.S0.data_ptr(), WB, m, m)
         finish_now = (k % self.every != 0)
         if fused and "cholinv" in self.fuse and m <= 16:
             # G = W0^T A W0 (A W0 never written) + A-CholQR factor S.  For m >= 32
@@ -447,8 +452,7 @@ class DeviceEngine:
                 "ekcg_update_vec", WB_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
                 part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
         else:
-            self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
-                         tag="tri_apply")
+            self._tri_apply(WB_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m)
             self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
         # m >= 32: the plane-marching stencil + xr_update beats the fused row kernel
         xr_fused = fused and "xr" in self.fuse and m <= 16
@@ -521,7 +525,7 @@ class DeviceEngine:
                 self._update(q_addr(0), m, d, m, C.data_ptr(), WA, m, WA, m, m, 1.0, -1.0, tag="hist_update")
         self._gram(WA_arr, m, 1, m, WA, m, m, self.Graw.data_ptr(), tag="gram_self")
         _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, self._karg(k), 1e-14, st)
-        self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, WC, m, m, 0.0, 1.0, tag="tri_apply")  # W0 -> WC
+        self._tri_apply(WA_arr, m, self.S0.data_ptr(), WC, m, m)  # W0 -> WC
         if fused and m <= 16:
             self._timed("spmm_gram", lambda: _lib.call(
                 "ekcg_stencil_cholinv", self.op.desc_ref(), WC, m, m, part.data_ptr(), self.counter.data_ptr(),
@@ -535,8 +539,7 @@ class DeviceEngine:
                 "ekcg_update_vec", WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m, n, self.r.data_ptr(),
                 part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st))
         else:
-            self._update(WC_arr, m, 1, m, self.S.data_ptr(), 0, m, blk.q.data_ptr(), m, m, 0.0, 1.0,
-                         tag="tri_apply")
+            self._tri_apply(WC_arr, m, self.S.data_ptr(), blk.q.data_ptr(), m, m)
             self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
         finish_now = (k % self.every != 0)
         xr_fused = fused and m <= 16

@@ -194,7 +194,7 @@ class ShardedEngine(DeviceEngine):
         self._gram(WA_arr, m, 1, m, lWA, m, m, self.Graw.data_ptr(), tag="gram_self")
         self.comm.allreduce_(self.Graw[: m * m])
         _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
-        self._update(WA_arr, m, 1, m, self.S0.data_ptr(), 0, m, lWB, m, m, 0.0, 1.0, tag="tri_apply")
+        self._tri_apply(WA_arr, m, self.S0.data_ptr(), lWB, m, m)
         self.comm.halo_exchange(self.WB, m, self.shard)
         fused = m in (8, 16, 32, 64)
         # same kernel choice as DeviceEngine: the fused stencil kernels only for
@@ -213,7 +213,7 @@ class ShardedEngine(DeviceEngine):
             _lib.call("ekcg_update_vec", WB_arr, m, self.S.data_ptr(), lq(blk), m, m, n, self.r.data_ptr(),
                       part.data_ptr(), self.counter.data_ptr(), self.alpha.data_ptr(), live, st)
         else:
-            self._update(WB_arr, m, 1, m, self.S.data_ptr(), 0, m, lq(blk), m, m, 0.0, 1.0, tag="tri_apply")
+            self._tri_apply(WB_arr, m, self.S.data_ptr(), lq(blk), m, m)
             self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
         self.comm.allreduce_(self.alpha[:m])
 

@@ -254,6 +254,24 @@ def test_wide_streamed_update_and_gram(m, d, n):
             assert (G[i] - gref).abs().max().item() <= 1e-13 * gscale
 
 
+@pytest.mark.parametrize("m", [3, 16, 32, 64])
+@pytest.mark.parametrize("n", [1, 1001, 70_003])
+def test_tri_apply(m, n):
+    """ekcg_tri_apply (W S, S upper triangular) equals the full block update bitwise
+    (the skipped blocks multiply exact zeros) and torch to 1e-13."""
+    rng = np.random.default_rng(m + n)
+    W = dev(rng.standard_normal((n, m)))
+    S = dev(np.triu(rng.standard_normal((m, m))))
+    tab = torch.tensor([W.data_ptr()], dtype=torch.int64, device=DEV)
+    out_tri, out_full = torch.empty_like(W), torch.empty_like(W)
+    _lib.call("ekcg_tri_apply", tab.data_ptr(), m, S.data_ptr(), out_tri.data_ptr(), m, m, n, None, stream())
+    _lib.call("ekcg_block_update", tab.data_ptr(), m, 1, m, S.data_ptr(), None, m, out_full.data_ptr(), m, m,
+              0.0, 1.0, n, None, stream())
+    assert torch.equal(out_tri, out_full)
+    scale = (W.abs() @ S.abs()).max().item() + 1.0
+    assert (out_tri - W @ S).abs().max().item() <= 1e-13 * scale
+
+
 @pytest.mark.parametrize("m", [1, 2, 6, 16, 64])
 def test_cholesky_and_trsm(m):
     rng = np.random.default_rng(m)
