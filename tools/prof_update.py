@@ -1,4 +1,4 @@
-"""One streamed m=16 block update for ncu: python tools/prof_update.py variant d"""
+"""One block update for ncu: python tools/prof_update.py variant d [m n]"""
 import sys
 
 import torch
@@ -7,7 +7,8 @@ sys.path.insert(0, ".")
 from paper_2305_19013_b200 import _lib  # noqa: E402
 
 var, d = int(sys.argv[1]), int(sys.argv[2])
-m, n = 16, 262144
+m = int(sys.argv[3]) if len(sys.argv) > 3 else 16
+n = int(sys.argv[4]) if len(sys.argv) > 4 else 262144
 st = torch.cuda.current_stream().cuda_stream
 Xs = [torch.randn(n * m, dtype=torch.float64, device="cuda") for _ in range(d)]
 W = torch.randn(n * m, dtype=torch.float64, device="cuda")
