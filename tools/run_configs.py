@@ -32,7 +32,7 @@ def main():
     ap.add_argument("--kmax-cfg3", type=int, default=None)
     ap.add_argument("--kmax-cfg4", type=int, default=400)
     ap.add_argument("--kmax-cfg5", type=int, default=20)
-    ap.add_argument("--repeats", type=int, default=2, help="best of N solves (the first pays one-time setup)")
+    ap.add_argument("--repeats", type=int, default=3, help="best of N solves (the first pays one-time setup)")
     ap.add_argument("--stencil-march", type=int, default=1, help="plane-marching stencil kernel (ekcg_tune 3)")
     args = ap.parse_args()
     from paper_2305_19013_b200 import _lib
