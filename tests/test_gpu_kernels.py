@@ -99,6 +99,27 @@ def test_stencil_equals_csr_bitwise(idx, edge, m):
     assert np.array_equal(pk.spmm(A, X), ref)
 
 
+@pytest.mark.parametrize("idx,edge", [(3, 32), (3, 40), (5, 128), (5, 96)])
+@pytest.mark.parametrize("m", [16, 32, 64])
+def test_march_tile_field_bitwise(idx, edge, m):
+    """Plane march on the config-3 / config-5 tile fields (per-tile coefficient fast
+    path for tile-interior nodes, face lookups elsewhere) against the reference
+    association on the assembled CSR, bitwise."""
+    prob = make_config(idx, edge, device_rhs=False)
+    A = prob.csr()
+    op = prob.stencil()
+    X = np.random.default_rng(idx + edge + m).standard_normal((prob.n, m))
+    Xd = dev(X)
+    Yd = torch.empty_like(Xd)
+    assert _lib.query("ekcg_tune", 12, 0) == 0  # march kernel at any size
+    try:
+        op.apply(Xd, m, Yd, m, m)
+    finally:
+        _lib.call("ekcg_tune", 12, 1 << 21)
+    ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, X)
+    assert np.array_equal(Yd.cpu().numpy().view(np.int64), ref.view(np.int64))
+
+
 @pytest.mark.parametrize("shape,kappa", [((17, 5, 9), None), ((67, 3), None), ((33, 33, 3), "tile"),
                                          ((2, 2, 2), None), ((130, 7), "node"), ((21, 19, 11), "node")])
 @pytest.mark.parametrize("m", [4, 12, 16, 20, 64])

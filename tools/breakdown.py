@@ -49,6 +49,9 @@ def main():
     b = torch.as_tensor(prob.b, device="cuda")
     res = None
     for rep in range(2):  # the first solve pays one-time setup
+        eng = None
+        hook = None
+        torch.cuda.empty_cache()
         eng = DeviceEngine(op, prob.partition, cfg)
         eng.no_fuse = args.no_fuse
         hook = Hook()
@@ -61,6 +64,8 @@ def main():
         s1.record()
         s1.synchronize()
         res = (s0.elapsed_time(s1), hook, rep_)
+        hook.engine = None
+        del eng, _
     total, hook, rep_ = res
     by = defaultdict(lambda: [0.0, 0])
     for tag, cur, e0, e1 in hook.used:
