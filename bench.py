@@ -9,7 +9,7 @@ complete solve to tol (111 iterations); value = iterations / device time.
 
 Under torchrun (N > 1) the rows are sharded across the ranks (one solve,
 strong scaling: halo exchange + NCCL allreduce, paper_2305_19013_b200/sharded.py);
-timing is the max over ranks.  --form csr falls back to independent replicas.
+timing is the max over ranks (stencil or CSR form).
 """
 
 from __future__ import annotations
@@ -241,7 +241,7 @@ def run_ours(args):
     timer = KernelTimer(torch, ["hist_gram", "hist_update"])
 
     from paper_2305_19013_b200.sharded import ShardedEngine
-    sharded = world > 1 and args.form == "stencil"
+    sharded = world > 1
 
     def solve_once(timed):
         if sharded:  # rows split across the ranks (strong scaling of one solve)

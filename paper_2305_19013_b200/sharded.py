@@ -13,7 +13,13 @@ kernel sequence as engine.DeviceEngine on its local rows:
 * the stencil kernels address rows globally (EkcgStencil.row_begin/row_end),
   so the same sm_100a kernels serve one GPU and a shard.
 
-Scope: stencil operators, SRE-CG2 / SRE-CG with s >= 1, full / trunc /
+General CSR matrices (the reference's SparseSpdMatrix) shard by balanced
+contiguous row ranges (dist.CsrShard): each rank keeps the local rows with
+column indices remapped into its extended block [lo halo | local | hi halo],
+and before each product receives exactly the off-slab rows its entries
+reference (one batched send/recv with every peer that owns some of them).
+
+Scope: stencil and CSR operators, SRE-CG2 / SRE-CG with s >= 1, full / trunc /
 restart retention (the cached-A Q scheme).
 """
 
@@ -25,40 +31,79 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dist import Comm, RowShard
+from .dist import Comm, CsrShard, RowShard
 from .engine import F64, DeviceEngine, _Block
-from .operators import StencilOperator
+from .operators import CsrOperator, StencilOperator
+
+
+class _LocalCsr:
+    """The local rows of a CsrShard as a CSR whose columns index the extended block."""
+
+    def __init__(self, A, shard):
+        e0, e1 = int(A.row_ptr[shard.row_begin]), int(A.row_ptr[shard.row_end])
+        self.n = shard.n_local
+        self.row_ptr = shard.local_row_ptr
+        self.col_idx = shard.local_col_idx
+        self.values = np.ascontiguousarray(np.asarray(A.values)[e0:e1], dtype=np.float64)
 
 
 class ShardedEngine(DeviceEngine):
     def __init__(self, op, partition, cfg, comm=None, device=None):
-        if not isinstance(op, StencilOperator):
-            raise TypeError("the sharded engine needs a StencilOperator")
         if cfg.preconditioner is not None:
             raise ValueError("the sharded engine runs unpreconditioned")
         if cfg.method not in ("sre-cg2", "sre-cg") or cfg.switch_tol is not None:
             raise ValueError("the sharded engine runs SRE-CG2 / SRE-CG without the flexible switch")
-        super().__init__(op, partition, cfg, device=device)
-        self.comm = comm if comm is not None else Comm()
-        self.shard = RowShard(op.shape, self.comm.rank, self.comm.world)
-        self.n_global = op.n
+        comm = comm if comm is not None else Comm()
+        self.stencil = isinstance(op, StencilOperator)
+        if self.stencil:
+            shard = RowShard(op.shape, comm.rank, comm.world)
+            local_op = op
+        else:
+            host = op.host if isinstance(op, CsrOperator) else op
+            if not all(hasattr(host, a) for a in ("n", "row_ptr", "col_idx", "values")):
+                raise TypeError("the sharded engine needs a StencilOperator or a CSR matrix")
+            shard = CsrShard(host.row_ptr, host.col_idx, comm.rank, comm.world).plan(comm)
+            local_op = CsrOperator(_LocalCsr(host, shard), device)
+        super().__init__(local_op, partition, cfg, device=device)
+        self.comm = comm
+        self.shard = shard
+        self.n_global = int(op.n)
         self.kmax = cfg.kmax if cfg.kmax is not None else 2 * self.n_global
         self.stag_window = max(20, self.kmax // 10) if self.retention == "restart" else 0
         self.n = self.shard.n_local  # every row-local kernel works on the local rows
         self.cache_aq = True
-        desc = _lib.EkcgStencil()
-        ctypes.memmove(ctypes.byref(desc), ctypes.byref(op._desc), ctypes.sizeof(desc))
-        desc.row_begin, desc.row_end = self.shard.row_begin, self.shard.row_end
-        self._desc = desc
+        if self.stencil:
+            desc = _lib.EkcgStencil()
+            ctypes.memmove(ctypes.byref(desc), ctypes.byref(op._desc), ctypes.sizeof(desc))
+            desc.row_begin, desc.row_end = self.shard.row_begin, self.shard.row_end
+            self._desc = desc
+        else:
+            self.send_idx = {q: torch.from_numpy(v).to(self.device) for q, v in shard.send.items()}
 
     # ------------------------------------------------------------ pointers
     def _lptr(self, ext, ld):
         """Local-row view of an extended (haloed) buffer."""
-        return ext.data_ptr() + F64 * self.shard.halo * ld
+        return ext.data_ptr() + F64 * self.shard.lo * ld
 
     def _gptr_ext(self, ext, ld):
-        """Global-row-addressed pointer into an extended buffer."""
+        """Global-row-addressed pointer into an extended buffer (stencil)."""
         return ext.data_ptr() + F64 * (self.shard.halo - self.shard.row_begin) * ld
+
+    def _exchange(self, ext, ld):
+        """Fill the halo rows of an extended block from the peers that own them."""
+        if self.stencil:
+            self.comm.halo_exchange(ext, ld, self.shard)
+        else:
+            self.comm.csr_exchange(ext, ld, self.shard, self.send_idx)
+
+    def _apply_ext(self, ext, col, ldx, y_loc, ldy, m, live):
+        """Y_local = A X for columns [col, col + m) of the extended block `ext`
+        (halos filled) into the local-row pointer y_loc."""
+        if self.stencil:
+            self._stencil(self._gptr_ext(ext, ldx) + F64 * col, ldx, y_loc - F64 * self.shard.row_begin * ldy, ldy,
+                          m, live)
+        else:
+            self.op.apply(ext.data_ptr() + F64 * col, ldx, y_loc, ldy, m, live, self.stream)
 
     def _gptr_loc(self, loc, ld):
         """Global-row-addressed pointer into a local (halo-free) buffer."""
@@ -107,7 +152,7 @@ class ShardedEngine(DeviceEngine):
             x0 = torch.as_tensor(x0, dtype=torch.float64)
             if x0.numel() == self.n_global:
                 x0 = x0[sh.row_begin:sh.row_end]
-            self.x[sh.halo:sh.halo + sh.n_local].copy_(x0.to(dev))
+            self.x[sh.lo:sh.lo + sh.n_local].copy_(x0.to(dev))
         self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
         self._residual_sq(self.x, self.rho2, None, store_r=True)
         _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
@@ -115,8 +160,8 @@ class ShardedEngine(DeviceEngine):
     def _residual_sq(self, x, out, live, store_r=False):
         """out = |b - A x|^2 over all ranks (x extended with halos)."""
         st = self.stream
-        self.comm.halo_exchange(x, 1, self.shard)
-        self._stencil(self._gptr_ext(x, 1), 1, self._gptr_loc(self.tmpv, 1), 1, 1, live)
+        self._exchange(x, 1)
+        self._apply_ext(x, 0, 1, self.tmpv.data_ptr(), 1, 1, live)
         dst = self.r if store_r else self.tmpv
         _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), dst.data_ptr(), self.n, live, st)
         _lib.call("ekcg_sumsq", dst.data_ptr(), self.n, self.vpart.data_ptr(), live, st)
@@ -130,7 +175,7 @@ class ShardedEngine(DeviceEngine):
         if x_star is not None:
             sh = self.shard
             xs = torch.as_tensor(x_star, dtype=torch.float64)[sh.row_begin:sh.row_end].to(self.device)
-            xl = self.x[sh.halo:sh.halo + sh.n_local]
+            xl = self.x[sh.lo:sh.lo + sh.n_local]
             sums = torch.stack([torch.sum((xl - xs) ** 2), torch.sum(xs ** 2)])
             self.comm.allreduce_(sums)
             rel = float(torch.sqrt(sums[0] / sums[1]).item())
@@ -138,7 +183,7 @@ class ShardedEngine(DeviceEngine):
 
     def _output_x(self, numpy_io):
         sh = self.shard
-        full = self.comm.gather_rows(self.x[sh.halo:sh.halo + sh.n_local].contiguous(), sh)
+        full = self.comm.gather_rows(self.x[sh.lo:sh.lo + sh.n_local].contiguous(), sh)
         return full.cpu().numpy() if numpy_io else full
 
     def _state(self, k, rho, tol1, numpy_io):
@@ -195,17 +240,17 @@ class ShardedEngine(DeviceEngine):
         self.comm.allreduce_(self.Graw[: m * m])
         _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
         self._tri_apply(WA_arr, m, self.S0.data_ptr(), lWB, m, m)
-        self.comm.halo_exchange(self.WB, m, self.shard)
+        self._exchange(self.WB, m)
         fused = m in (8, 16, 32, 64)
         # same kernel choice as DeviceEngine: the fused stencil kernels only for
-        # m <= 16, the plane-marching stencil + DMMA kernels above
-        fused_st = fused and m <= 16
+        # m <= 16, the plane-marching stencil + DMMA kernels above (CSR: unfused)
+        fused_st = fused and m <= 16 and self.stencil
         part = self._ensure("part", max(self.fused_part, 1)) if fused else None
         if fused_st:
             _lib.call("ekcg_stencil_cholinv", ctypes.byref(self._desc), self._gptr_ext(self.WB, m), m, m,
                       part.data_ptr(), self.counter.data_ptr(), self.G.data_ptr(), live, k, 1e-14, 0, st)
         else:
-            self._stencil(self._gptr_ext(self.WB, m), m, self._gptr_loc(self.WC, m), m, m, live)
+            self._apply_ext(self.WB, 0, m, self.WC.data_ptr(), m, m, live)
             self._gram(WB_arr, m, 1, m, self.WC.data_ptr(), m, m, self.G.data_ptr(), tag="gram_self")
         self.comm.allreduce_(self.G[: m * m])
         _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
@@ -218,14 +263,14 @@ class ShardedEngine(DeviceEngine):
         self.comm.allreduce_(self.alpha[:m])
 
         # ---- AW_k = A W_k and the iterate update ----
-        self.comm.halo_exchange(blk.q, m, self.shard)
+        self._exchange(blk.q, m)
         if fused_st:
             _lib.call("ekcg_stencil_xr", ctypes.byref(self._desc), self._gptr_ext(blk.q, m), m,
                       self._gptr_loc(blk.aq, m), m, m, self.alpha.data_ptr(), self._gptr_ext(self.x, 1),
                       self._gptr_loc(self.r, 1), part.data_ptr(), self.counter.data_ptr(), live, k, self.kmax,
                       self.stag_window, self.history.data_ptr(), 0, self.rho2.data_ptr(), st)
         else:
-            self._stencil(self._gptr_ext(blk.q, m), m, self._gptr_loc(blk.aq, m), m, m, live)
+            self._apply_ext(blk.q, 0, m, blk.aq.data_ptr(), m, m, live)
             _lib.call("ekcg_xr_update", lq(blk), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
                       self._lptr(self.x, 1), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st)
             _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
@@ -242,7 +287,6 @@ class ShardedEngine(DeviceEngine):
         self._account(k, d, m, fresh, t)
 
     def _chain_sharded(self, m, t, live):
-        g = lambda col: self._gptr_ext(self.WA, m) + F64 * col
         for i in range(1, self.s):
-            self.comm.halo_exchange(self.WA, m, self.shard)
-            self._stencil(g((i - 1) * t), m, g(i * t), m, t, live)
+            self._exchange(self.WA, m)
+            self._apply_ext(self.WA, (i - 1) * t, m, self._lptr(self.WA, m) + F64 * i * t, m, t, live)

@@ -247,7 +247,8 @@ def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iter
     import torch.distributed as tdist
     from .operators import StencilOperator
     sharded = (tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1
-               and isinstance(A, StencilOperator))
+               and F is None and cfg.method in ("sre-cg2", "sre-cg") and cfg.switch_tol is None
+               and (isinstance(A, StencilOperator) or hasattr(A, "row_ptr") or hasattr(A, "host")))
     if sharded:  # one process per GPU, rows split across ranks
         from .sharded import ShardedEngine
         engine = ShardedEngine(A, partition, cfg, device=device)

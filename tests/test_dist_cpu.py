@@ -15,7 +15,8 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2305_19013_b200.dist import Comm, RowShard
+from oracle import ekcg_oracle as orc
+from paper_2305_19013_b200.dist import Comm, CsrShard, RowShard, row_bounds
 from paper_2305_19013_b200.problems import diffusion_csr
 
 
@@ -98,3 +99,83 @@ def test_row_shard_covers_rows(layers, world):
     assert not shards[0].has_lo and not shards[-1].has_hi
     with pytest.raises(ValueError):
         RowShard((4, 4), 0, 5)
+
+
+def _random_spd_csr(n, rng):
+    """Symmetric sparsity with far-off columns (non-banded) and a dominant diagonal."""
+    rows, cols = [], []
+    for i in range(n):
+        k = rng.integers(1, 6)
+        js = rng.choice(n, k, replace=False)
+        for j in js:
+            if j != i:
+                rows += [i, j]
+                cols += [j, i]
+    M = np.zeros((n, n))
+    M[rows, cols] = rng.uniform(-1, 0, len(rows))
+    M = 0.5 * (M + M.T)
+    M[np.arange(n), np.arange(n)] = np.abs(M).sum(axis=1) + 1.0
+    rp = np.concatenate(([0], np.cumsum((M != 0).sum(axis=1)))).astype(np.int64)
+    ci = np.nonzero(M)[1].astype(np.int64)
+    return rp, ci, M[M != 0]
+
+
+def _csr_worker(rank, world, port, kind, m, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = Comm()
+        rng = np.random.default_rng(11)
+        if kind == "grid":
+            A = diffusion_csr((5, 4, 6), np.exp(rng.uniform(-2, 2, 120)))
+            rp, ci, vals = A.row_ptr, A.col_idx, A.values
+        else:
+            rp, ci, vals = _random_spd_csr(90, rng)
+        n = len(rp) - 1
+        X = rng.standard_normal((n, m))
+        sh = CsrShard(rp, ci, rank, world).plan(comm)
+        ext = torch.zeros(sh.ext_rows * m, dtype=torch.float64)
+        ext.view(sh.ext_rows, m)[sh.lo:sh.lo + sh.n_local] = torch.from_numpy(X[sh.row_begin:sh.row_end])
+        comm.csr_exchange(ext, m, sh, {q_: torch.from_numpy(v) for q_, v in sh.send.items()})
+        E = ext.view(sh.ext_rows, m).numpy()
+        halo_ok = (np.array_equal(E[:sh.lo], X[sh.lo_rows]) and
+                   np.array_equal(E[sh.lo + sh.n_local:], X[sh.hi_rows]))
+        e0, e1 = rp[sh.row_begin], rp[sh.row_end]
+        lci = sh.local_col_idx.astype(np.int64)
+        Y_loc = np.add.reduceat(vals[e0:e1][:, None] * E[lci], sh.local_row_ptr[:-1], axis=0)  # linalg.py:150
+        Y_ref = orc.csr_spmm(rp, ci, vals, X)[sh.row_begin:sh.row_end]
+        prod_ok = np.array_equal(Y_loc.view(np.int64), Y_ref.view(np.int64))  # same association: bitwise
+        full = comm.gather_rows(torch.from_numpy(X[sh.row_begin:sh.row_end, 0].copy()), sh)
+        gather_ok = np.array_equal(full.numpy(), X[:, 0])
+        q.put((rank, bool(halo_ok), bool(prod_ok), bool(gather_ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,kind", [(2, "grid"), (3, "grid"), (2, "random"), (3, "random")])
+def test_csr_sharded_dataflow_gloo(world, kind):
+    """CSR row shards: the halo plan (requests exchanged once), the per-product exchange
+    and a local product on [lo halo | local | hi halo] that equals the global rows bitwise."""
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    port = _free_port()
+    procs = [ctx.Process(target=_csr_worker, args=(r, world, port, kind, 4, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    for rank, halo_ok, prod_ok, gather_ok in sorted(q.get() for _ in range(world)):
+        assert halo_ok and prod_ok and gather_ok, (rank, halo_ok, prod_ok, gather_ok)
+
+
+def test_csr_shard_single_rank_and_bounds():
+    rp, ci, vals = _random_spd_csr(40, np.random.default_rng(2))
+    sh = CsrShard(rp, ci, 0, 1)
+    assert sh.lo == 0 and sh.ext_rows == 40 and not sh.recv
+    assert np.array_equal(sh.local_col_idx, ci) and np.array_equal(sh.local_row_ptr, rp)
+    b = row_bounds(10, 3)
+    assert list(b) == [0, 4, 7, 10]
+    with pytest.raises(ValueError):
+        row_bounds(2, 3)

@@ -310,14 +310,15 @@ def test_lean_scheme_matches_cached(floors_golden, solves_golden, idx, edge, for
 
 @pytest.mark.parametrize("idx,edge,over", [(2, 16, {}), (3, 16, {}), (4, 10, {}), (1, 40, {}),
                                            (2, 12, {"retention": "restart", "restart_j": 5})])
-def test_sharded_engine_single_rank_matches(idx, edge, over):
-    """The row-sharded engine (halo'd blocks, global-row stencil addressing,
-    allreduce points) on one rank follows the single-GPU engine."""
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+def test_sharded_engine_single_rank_matches(idx, edge, over, form):
+    """The row-sharded engine (halo'd blocks, global-row stencil addressing or the
+    remapped local CSR, allreduce points) on one rank follows the single-GPU engine."""
     from paper_2305_19013_b200.engine import DeviceEngine
     from paper_2305_19013_b200.sharded import ShardedEngine
     prob = make_config(idx, edge)
     cfg = SolverConfig(**dict(prob.solver_kwargs, **over))
-    op = prob.stencil()
+    op = prob.stencil() if form == "stencil" else prob.csr()
     _, ref = DeviceEngine(op, prob.partition, cfg).solve(prob.b, x_star=prob.x_star)
     x, rep = ShardedEngine(op, prob.partition, cfg).solve(prob.b, x_star=prob.x_star)
     assert rep.status == ref.status
