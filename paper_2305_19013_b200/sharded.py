@@ -20,7 +20,8 @@ and before each product receives exactly the off-slab rows its entries
 reference (one batched send/recv with every peer that owns some of them).
 
 Scope: stencil and CSR operators, SRE-CG2 / SRE-CG with s >= 1, full / trunc /
-restart retention (the cached-A Q scheme).
+restart retention; the cached-A Q scheme, or the lean one (no A Q cache, one
+operator application per CGS2 pass) when the cached blocks do not fit.
 """
 
 from __future__ import annotations
@@ -71,7 +72,7 @@ class ShardedEngine(DeviceEngine):
         self.kmax = cfg.kmax if cfg.kmax is not None else 2 * self.n_global
         self.stag_window = max(20, self.kmax // 10) if self.retention == "restart" else 0
         self.n = self.shard.n_local  # every row-local kernel works on the local rows
-        self.cache_aq = True
+        self.cache_aq = "auto"  # the lean scheme when the cached one does not fit the local HBM
         if self.stencil:
             desc = _lib.EkcgStencil()
             ctypes.memmove(ctypes.byref(desc), ctypes.byref(op._desc), ctypes.sizeof(desc))
@@ -119,7 +120,11 @@ class ShardedEngine(DeviceEngine):
         mm = self.m_max
         f64 = dict(dtype=torch.float64, device=self.device)
         self.WA = torch.zeros(ext * mm, **f64)   # candidate / s-step chain (stencil input)
-        self.WB = torch.zeros(ext * mm, **f64)   # W0 (stencil input)
+        if self.lean:  # WC carries A W, then W0 (stencil input); no WB
+            self.WB = torch.empty(0, **f64)
+            self.WC = torch.zeros(ext * mm, **f64)
+        else:
+            self.WB = torch.zeros(ext * mm, **f64)   # W0 (stencil input)
         self.fused_ok = True
         owner = self.partition.owner()[self.shard.row_begin:self.shard.row_end]
         self.owner_dev = torch.from_numpy(np.ascontiguousarray(owner, dtype=np.int32)).to(self.device)
@@ -130,7 +135,8 @@ class ShardedEngine(DeviceEngine):
         if self.window is not None:
             slot = self.since_clear % self.window
             if slot not in self.slots:
-                self.slots[slot] = (torch.zeros(ext * self.m_max, **f64), torch.empty(self.n * self.m_max, **f64))
+                aq = None if self.lean else torch.empty(self.n * self.m_max, **f64)
+                self.slots[slot] = (torch.zeros(ext * self.m_max, **f64), aq)
             q, aq = self.slots[slot]
         else:
             slot = -1
@@ -190,7 +196,69 @@ class ShardedEngine(DeviceEngine):
         raise NotImplementedError("on_iteration callbacks are not available on the sharded engine")
 
     # ----------------------------------------------------------- iteration
+    def _enqueue_iteration_lean(self, k, tol1):
+        """engine._enqueue_iteration_lean on a shard: w Q blocks + WA / WC, one
+        operator application (with its halo exchange) per CGS2 pass."""
+        cfg, n, st, live = self.cfg, self.n, self.stream, self.live
+        if k > 1 and self.retention == "restart" and k % cfg.restart_j == 1:
+            self._clear()
+            self.restarts.append(k)
+        elif (k > 1 and self.retention == "restart-tol" and tol1 < cfg.restart_tol
+              and (not self.restarts or k > self.restarts[-1] + 1)):
+            self._clear()
+            self.restarts.append(k)
+        m = t = self.t_cur
+        d = len(self.retained)
+        self._cur = (k, d, m)
+        blk = self._new_block(m)
+        lWA, lWC = self._lptr(self.WA, m), self._lptr(self.WC, m)
+        lq = lambda b: self._lptr(b.q, b.width)
+        base = self.arena.push([lq(b) for b in self.retained] + [lWA, lWC, lq(blk)])
+        q_addr = lambda i: base + F64 * i
+        WA_arr, WC_arr, NEW_arr = (base + F64 * (d + j) for j in range(3))
+        fresh = not self.retained
+        if fresh:
+            _lib.call("ekcg_split", self.r.data_ptr(), self.owner_dev.data_ptr(), lWA, n, t, m, live, st)
+        if d > 0:
+            C = self._ensure("C", d * m * m)
+            for _ in range(2):  # C = Q^T (A W), A symmetric (engine._enqueue_iteration_lean)
+                self._exchange(self.WA, m)
+                self._apply_ext(self.WA, 0, m, lWC, m, m, live)
+                self._gram(q_addr(0), m, d, m, lWC, m, m, C.data_ptr(), tag="hist_gram")
+                self.comm.allreduce_(C[: d * m * m])
+                self._update(q_addr(0), m, d, m, C.data_ptr(), lWA, m, lWA, m, m, 1.0, -1.0, tag="hist_update")
+        self._gram(WA_arr, m, 1, m, lWA, m, m, self.Graw.data_ptr(), tag="gram_self")
+        self.comm.allreduce_(self.Graw[: m * m])
+        _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
+        self._tri_apply(WA_arr, m, self.S0.data_ptr(), lWC, m, m)  # W0 -> WC
+        self._exchange(self.WC, m)
+        self._apply_ext(self.WC, 0, m, lWA, m, m, live)  # A W0 -> WA (free)
+        self._gram(WC_arr, m, 1, m, lWA, m, m, self.G.data_ptr(), tag="gram_self")
+        self.comm.allreduce_(self.G[: m * m])
+        _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
+        self._tri_apply(WC_arr, m, self.S.data_ptr(), lq(blk), m, m)
+        self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
+        self.comm.allreduce_(self.alpha[:m])
+        self._exchange(blk.q, m)
+        self._apply_ext(blk.q, 0, m, lWA, m, m, live)  # A W_k -> WA: the next candidate
+        _lib.call("ekcg_xr_update", lq(blk), m, lWA, m, self.alpha.data_ptr(), m, self._lptr(self.x, 1),
+                  self.r.data_ptr(), n, self.vpart.data_ptr(), live, st)
+        _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
+        self.comm.allreduce_(self.rho2)
+        self._append(blk)
+        if k % self.every == 0:
+            slot = k // self.every - 1
+            self._ensure_checks(slot + 1)
+            self._residual_sq(self.x, self.tr2, live)
+            _lib.call("ekcg_store_norm", self.tr2.data_ptr(), self.checks.data_ptr(), slot, live, st)
+        self._ensure_history(k + 1)
+        _lib.call("ekcg_finish", self.ctrl.data_ptr(), self.rho2.data_ptr(), k, self.kmax, self.stag_window,
+                  self.history.data_ptr(), st)
+        self._account(k, d, m, fresh, t)
+
     def _enqueue_iteration(self, k, tol1):
+        if self.lean:
+            return self._enqueue_iteration_lean(k, tol1)
         cfg, n, st, live = self.cfg, self.n, self.stream, self.live
         if k > 1 and self.retention == "restart" and k % cfg.restart_j == 1:
             self._clear()

@@ -351,3 +351,26 @@ def test_graph_replay_matches_direct_launches(idx, edge):
     assert np.array_equal(xa, xb)
     assert a.peak_block_vectors == b.peak_block_vectors
     assert [c[0] for c in a.true_residual_checks] == [c[0] for c in b.true_residual_checks]
+
+
+@pytest.mark.parametrize("idx,edge,form", [(3, 16, "stencil"), (5, 64, "stencil"), (3, 16, "csr"), (1, 40, "csr")])
+def test_sharded_lean_scheme_single_rank_matches(idx, edge, form):
+    """The sharded engine's lean scheme (no A Q cache, one operator application per
+    CGS2 pass, as chosen when the cached blocks do not fit) against the
+    single-GPU lean engine."""
+    from paper_2305_19013_b200.engine import DeviceEngine
+    from paper_2305_19013_b200.sharded import ShardedEngine
+    prob = make_config(idx, edge)
+    cfg = SolverConfig(**prob.solver_kwargs)
+    op = prob.stencil() if form == "stencil" else prob.csr()
+    ref_eng = DeviceEngine(op, prob.partition, cfg)
+    ref_eng.cache_aq = False
+    _, ref = ref_eng.solve(prob.b)
+    eng = ShardedEngine(op, prob.partition, cfg)
+    eng.cache_aq = False
+    x, rep = eng.solve(prob.b)
+    assert eng.lean and ref_eng.lean
+    assert rep.status == ref.status
+    assert abs(rep.iterations - ref.iterations) <= max(1, round(0.02 * ref.iterations))
+    assert hist_dev(rep.residual_history, ref.residual_history) <= 1e-8
+    assert rep.peak_block_vectors == ref.peak_block_vectors or rep.iterations != ref.iterations
