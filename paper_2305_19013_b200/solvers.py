@@ -248,6 +248,7 @@ def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iter
     from .operators import StencilOperator
     sharded = (tdist.is_available() and tdist.is_initialized() and tdist.get_world_size() > 1
                and F is None and cfg.method in ("sre-cg2", "sre-cg") and cfg.switch_tol is None
+               and on_iteration is None  # callbacks see whole blocks: the single-GPU engine serves them
                and (isinstance(A, StencilOperator) or hasattr(A, "row_ptr") or hasattr(A, "host")))
     if sharded:  # one process per GPU, rows split across ranks
         from .sharded import ShardedEngine
