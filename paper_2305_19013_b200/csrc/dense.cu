@@ -145,6 +145,13 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
 
     const int lr = lane & 3;
     const int lc = lane >> 2;
+    // X^T X (the Pre-CholQR Gram W^T W, aortho.py:105): the quadrant below the
+    // diagonal is the transpose of the one above it -- same products, same
+    // order -- so its warp skips the DMMAs and the mirror warp stores both.
+    constexpr int QB = M / 8 / TB;
+    const bool sym = QA == 2 && QB == 2 && KS == 1 && GB == 1 && d == 1 && X[0] == Y;
+    const int qa = quad % QA, qb = quad / QA;
+    if (sym && qa > qb) return;  // no block barrier follows when KS == 1
     for (long long s0 = ks; s0 < steps; s0 += (long long)KS * U) {
         double af[U][GB][TA], bf[U][TB];
 #pragma unroll
@@ -176,8 +183,13 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
 #pragma unroll
                 for (int tb = 0; tb < TB; ++tb) {
                     const int a = a_base + tile_col<TA, IL>(ta, lc);
-                    out[a * M + b_base + tile_col<TB, IL>(tb, 2 * lr)] = acc[g][ta][tb][0];
-                    out[a * M + b_base + tile_col<TB, IL>(tb, 2 * lr + 1)] = acc[g][ta][tb][1];
+                    const int b0 = b_base + tile_col<TB, IL>(tb, 2 * lr), b1 = b_base + tile_col<TB, IL>(tb, 2 * lr + 1);
+                    out[a * M + b0] = acc[g][ta][tb][0];
+                    out[a * M + b1] = acc[g][ta][tb][1];
+                    if (sym && qa < qb) {
+                        out[b0 * M + a] = acc[g][ta][tb][0];
+                        out[b1 * M + a] = acc[g][ta][tb][1];
+                    }
                 }
         }
     } else {

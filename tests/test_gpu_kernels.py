@@ -207,6 +207,27 @@ def test_gram_multi_block(m1, m2, n):
         assert (got[i] - ref).abs().max().item() <= 1e-13 * scale
 
 
+@pytest.mark.parametrize("n", [37, 4099, 200_000])
+def test_gram_self_symmetric_shortcut(n):
+    """X^T X at m = 64 (the Pre-CholQR Gram) skips the quadrant below the diagonal
+    and mirrors the one above: bitwise equal to X^T Y with Y a copy of X."""
+    m = 64
+    X = dev(np.random.default_rng(n).standard_normal((n, m)))
+    Xc = X.clone()
+    tab = torch.tensor([X.data_ptr()], dtype=torch.int64, device=DEV)
+    chunks = _lib.query("ekcg_gram_chunks", n, 1, m, m)
+    outs = []
+    for Y in (X, Xc):
+        part = torch.empty(chunks * m * m, dtype=torch.float64, device=DEV)
+        G = torch.empty(m * m, dtype=torch.float64, device=DEV)
+        _lib.call("ekcg_gram", tab.data_ptr(), m, 1, m, Y.data_ptr(), m, m, n, part.data_ptr(), None, stream())
+        _lib.call("ekcg_reduce", part.data_ptr(), chunks, m * m, G.data_ptr(), None, stream())
+        outs.append(G.view(m, m))
+    assert torch.equal(outs[0], outs[1])
+    assert torch.equal(outs[0], outs[0].T)
+    assert (outs[0] - X.T @ X).abs().max().item() <= 1e-13 * (X.abs().T @ X.abs()).max().item()
+
+
 def test_gram_deterministic():
     rng = np.random.default_rng(9)
     X = rng.standard_normal((300_001, 16))
