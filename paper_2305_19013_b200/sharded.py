@@ -129,6 +129,14 @@ class ShardedEngine(DeviceEngine):
         owner = self.partition.owner()[self.shard.row_begin:self.shard.row_end]
         self.owner_dev = torch.from_numpy(np.ascontiguousarray(owner, dtype=np.int32)).to(self.device)
 
+    def _choose_lean(self, n, m):
+        """The cached / lean decision must be the same on every rank (the
+        schemes issue different collectives): lean if any rank needs it."""
+        lean = super()._choose_lean(n, m)
+        flag = torch.tensor([1.0 if lean else 0.0], dtype=torch.float64, device=self.device)
+        self.comm.max_(flag)
+        return bool(flag.item() > 0.0)
+
     def _new_block(self, width):
         ext = self.shard.ext_rows
         f64 = dict(dtype=torch.float64, device=self.device)
