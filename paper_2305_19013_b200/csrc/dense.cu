@@ -34,6 +34,7 @@ long long g_gram_target = 0;  // 0: automatic
 int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
                        int chunks, long long rows_chunk, double* partials, const int* live, cudaStream_t st);
 extern int g_gram_stream;
+extern int g_gram16_d1;
 int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
                          double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                          cudaStream_t st);
@@ -281,8 +282,9 @@ int gram_chunks(long long n, int d, int m1, int m2) {
         // streamed Gram: resident CTAs with long row ranges.  Pick the chunk
         // count whose CTA total fills its last wave best (equal work per CTA),
         // preferring fewer chunks; at least 1024 rows per chunk.
-        const long long slots = wide ? gram_wide_slots(gb) : 148;
-        long long pmax = (n + 1023) / 1024;
+        const bool d1 = !wide && d == 1 && g_gram16_d1;  // GB = 1 stream kernel: 3 CTAs per SM
+        const long long slots = wide ? gram_wide_slots(gb) : d1 ? 3 * 148 : 148;
+        long long pmax = (n + (d1 ? 511 : 1023)) / (d1 ? 512 : 1024);
         const long long cap = (4 * slots + groups - 1) / groups;
         if (pmax > cap) pmax = cap;
         if (pmax < 1) pmax = 1;
@@ -879,6 +881,10 @@ extern "C" int ekcg_tune(int key, long long value) {
     }
     if (key == 17 && value >= 0 && value <= 2) {
         g_csr_vec = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 21 && value >= 0 && value <= 4) {
+        g_gram16_d1 = (int)value;
         return EKCG_OK;
     }
     if (key == 16 && value >= 0 && value <= 2) {

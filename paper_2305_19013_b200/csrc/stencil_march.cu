@@ -193,7 +193,10 @@ stencil_march_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil s, Un
             mbar_wait(&bar[(q + 1) % kNS], ((q + 1) / kNS) & 1);
         }
         __syncthreads();
-        if (tid == 0 && q + kAhead < nq) issue(q + kAhead);
+        if (tid == 0 && q + kAhead < nq) {
+            fence_proxy_async_smem();  // the CTA's generic reads of the stage (ordered by the barrier) before the refill
+            issue(q + kAhead);
+        }
         const double* pm = smem + ((q - 1) % kNS) * P::STAGE;
         const double* pc = smem + (q % kNS) * P::STAGE;
         const double* pp = smem + ((q + 1) % kNS) * P::STAGE;
@@ -375,8 +378,10 @@ stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil
             if (DIM == 3) tma_load_4d(smem + slot * P::STAGE, &tmap, &bar[slot], 0, x0 - 1, y0 - 1, z);
             else tma_load_3d(smem + slot * P::STAGE, &tmap, &bar[slot], 0, x0 - 1, z);
         };
-        if (tid == 0)
+        if (tid == 0) {
+            fence_proxy_async_smem();  // the previous item's generic reads of the stages before the refills
             for (int q = 0; q <= kAhead && q < nq; ++q) issue(q);
+        }
         const bool act = (x0 + ix < (int)nx) && (DIM == 2 || y0 + iy < (int)ny);
         for (int w = wb; w < we; ++w) {
             const int q = w - wb + 1;
@@ -388,7 +393,10 @@ stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil
                 mbar_wait(&bar[(qg + q + 1) % kNS], (unsigned)(((qg + q + 1) / kNS) & 1));
             }
             __syncthreads();
-            if (tid == 0 && q + kAhead < nq) issue(q + kAhead);
+            if (tid == 0 && q + kAhead < nq) {
+                fence_proxy_async_smem();  // the CTA's generic reads of the stage (ordered by the barrier) before the refill
+                issue(q + kAhead);
+            }
             const double* pm = smem + ((qg + q - 1) % kNS) * P::STAGE;
             const double* pc = smem + ((qg + q) % kNS) * P::STAGE;
             const double* pp = smem + ((qg + q + 1) % kNS) * P::STAGE;

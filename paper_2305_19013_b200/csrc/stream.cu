@@ -51,6 +51,8 @@ gram16_stream_kernel(const double* const* __restrict__ Xs, int d, const double* 
     }
     __syncthreads();
 
+    // a block with itself (the Pre-CholQR Gram W^T W): stream it once, read it as both operands
+    const bool self_gram = GB == 1 && d == 1 && Xs[0] == Y;
     if (warp == 4) {  // producer
         if (lane == 0) {
             const double* X[GB];
@@ -58,19 +60,25 @@ gram16_stream_kernel(const double* const* __restrict__ Xs, int d, const double* 
             for (int g = 0; g < GB; ++g) X[g] = Xs[min(i0 + g, d - 1)];
             for (int j = 0; j < nsteps; ++j) {
                 const int slot = j % NS;
-                if (j >= NS) mbar_wait(&empty[slot], ((j / NS) - 1) & 1);
+                if (j >= NS) {
+                    mbar_wait(&empty[slot], ((j / NS) - 1) & 1);
+                    fence_proxy_async_smem();  // the consumers' generic reads of the slot before the TMA write
+                }
                 const long long rb = r0 + (long long)j * R;
                 const unsigned bytes = (unsigned)(min((long long)R, r1 - rb) * M * sizeof(double));
-                mbar_expect_tx(&full[slot], bytes * (unsigned)(nb + 1));
+                mbar_expect_tx(&full[slot], bytes * (unsigned)(self_gram ? 1 : nb + 1));
                 double* st = sm + slot * P::STAGE;
                 bulk_load(st, Y + rb * M, bytes, &full[slot]);
+                if (!self_gram) {
 #pragma unroll
-                for (int g = 0; g < GB; ++g)
-                    if (g < nb) bulk_load(st + (g + 1) * P::SLAB, X[g] + rb * M, bytes, &full[slot]);
+                    for (int g = 0; g < GB; ++g)
+                        if (g < nb) bulk_load(st + (g + 1) * P::SLAB, X[g] + rb * M, bytes, &full[slot]);
+                }
             }
         }
         return;
     }
+    const int xoff = self_gram ? 0 : P::SLAB;  // X_g slab: (g + 1) * SLAB, or the Y slab itself
 
     const int lr = lane & 3, lc = lane >> 2;
     double acc[GB][2][2][2];
@@ -94,7 +102,7 @@ gram16_stream_kernel(const double* const* __restrict__ Xs, int d, const double* 
 #pragma unroll
             for (int g = 0; g < GB; ++g) {
                 const double2 a = (ok && g < nb)
-                                      ? *reinterpret_cast<const double2*>(st + (g + 1) * P::SLAB + row * M + 2 * lc)
+                                      ? *reinterpret_cast<const double2*>(st + g * P::SLAB + xoff + row * M + 2 * lc)
                                       : make_double2(0.0, 0.0);
                 dmma_8x8x4(acc[g][0][0], a.x, b.x);
                 dmma_8x8x4(acc[g][0][1], a.x, b.y);
@@ -191,7 +199,10 @@ update16_stream_kernel(const double* const* __restrict__ Qs, int d, const double
                 const unsigned bytes = (unsigned)(min((long long)R, n - rb) * M * sizeof(double));
                 for (int i = 0; i < d; ++i, ++t) {
                     const int slot = (int)(t % NS);
-                    if (t >= NS) mbar_wait(&empty[slot], (unsigned)(((t / NS) - 1) & 1));
+                    if (t >= NS) {
+                        mbar_wait(&empty[slot], (unsigned)(((t / NS) - 1) & 1));
+                        fence_proxy_async_smem();  // the consumers' generic reads of the slot before the TMA write
+                    }
                     mbar_expect_tx(&full[slot], bytes + (unsigned)(M * M * sizeof(double)));
                     bulk_load(sm + slot * SLOT, Qs[i] + rb * M, bytes, &full[slot]);
                     bulk_load(sm + slot * SLOT + SLAB, C + (long long)i * M * M, M * M * sizeof(double), &full[slot]);
@@ -289,6 +300,7 @@ int launch_update16_stream(const double* const* Qs, int d, const double* C, cons
 }  // namespace
 
 int g_gram_stream = 3;  // ekcg_tune key 7: streamed Gram for 16-column blocks, 0 off, 1.. variants
+int g_gram16_d1 = 1;    // ekcg_tune key 21: one-block (d = 1) streamed Gram with GB = 1 (3 CTAs per SM)
 
 // Streamed Gram when it applies (16 contiguous columns, aligned); EKCG_EINVAL otherwise.
 int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
@@ -296,6 +308,7 @@ int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const do
     if (!g_gram_stream || m1 != 16 || m2 != 16 || ldx != 16 || ldy != 16 || (reinterpret_cast<uintptr_t>(Y) & 15) ||
         rows_chunk % 16 != 0)
         return EKCG_EINVAL;
+    if (d == 1 && g_gram16_d1) return launch_gram16_stream<1, 64, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
     switch (g_gram_stream) {
         case 2: return launch_gram16_stream<4, 32, 6>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
         case 3: return launch_gram16_stream<4, 64, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);

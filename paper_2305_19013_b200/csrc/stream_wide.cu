@@ -73,7 +73,10 @@ gram_wide_stream_kernel(const double* const* __restrict__ Xs, int d, const doubl
             for (int g = 0; g < GB; ++g) X[g] = Xs[min(i0 + g, d - 1)];
             for (int j = 0; j < nsteps; ++j) {
                 const int slot = j % NS;
-                if (j >= NS) mbar_wait(&empty[slot], ((j / NS) - 1) & 1);
+                if (j >= NS) {
+                    mbar_wait(&empty[slot], ((j / NS) - 1) & 1);
+                    fence_proxy_async_smem();  // the consumers' generic reads of the slot before the TMA write
+                }
                 const long long rb = r0 + (long long)j * R;
                 const unsigned bytes = (unsigned)(min((long long)R, r1 - rb) * M * sizeof(double));
                 mbar_expect_tx(&full[slot], bytes * (unsigned)(nb + 1));
@@ -213,7 +216,10 @@ update_wide_stream_kernel(const double* const* __restrict__ Qs, int d, const dou
                 const unsigned bytes = (unsigned)(min((long long)R, n - rb) * M * sizeof(double));
                 for (int i = 0; i < d; ++i, ++t) {
                     const int slot = (int)(t % NS);
-                    if (t >= NS) mbar_wait(&empty[slot], (unsigned)(((t / NS) - 1) & 1));
+                    if (t >= NS) {
+                        mbar_wait(&empty[slot], (unsigned)(((t / NS) - 1) & 1));
+                        fence_proxy_async_smem();  // the consumers' generic reads of the slot before the TMA write
+                    }
                     mbar_expect_tx(&full[slot], bytes);
                     bulk_load(sm + slot * P::SLAB, Qs[i] + rb * M, bytes, &full[slot]);
                 }

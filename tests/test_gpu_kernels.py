@@ -208,10 +208,11 @@ def test_gram_multi_block(m1, m2, n):
 
 
 @pytest.mark.parametrize("n", [37, 4099, 200_000])
-def test_gram_self_symmetric_shortcut(n):
-    """X^T X at m = 64 (the Pre-CholQR Gram) skips the quadrant below the diagonal
-    and mirrors the one above: bitwise equal to X^T Y with Y a copy of X."""
-    m = 64
+@pytest.mark.parametrize("m", [16, 64])
+def test_gram_self_symmetric_shortcut(n, m):
+    """X^T X (the Pre-CholQR Gram): at m = 64 the quadrant below the diagonal mirrors
+    the one above, at m = 16 the block is streamed once and read as both operands;
+    bitwise equal to X^T Y with Y a copy of X."""
     X = dev(np.random.default_rng(n).standard_normal((n, m)))
     Xc = X.clone()
     tab = torch.tensor([X.data_ptr()], dtype=torch.int64, device=DEV)
@@ -226,6 +227,29 @@ def test_gram_self_symmetric_shortcut(n):
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(outs[0], outs[0].T)
     assert (outs[0] - X.T @ X).abs().max().item() <= 1e-13 * (X.abs().T @ X.abs()).max().item()
+
+
+@pytest.mark.parametrize("target", [296, 444, 592])
+def test_streamed_gram_many_ctas_per_sm(target):
+    """Regression: the TMA ring refills a slot only after a proxy fence orders the
+    consumers' generic reads before the async write.  Without it, 3+ co-resident
+    CTAs per SM (the one-block m = 16 Gram at these chunk counts) read refilled
+    slots and ~1 % of the rows went wrong."""
+    n, m = 200_000, 16
+    X = torch.randn(n, m, dtype=torch.float64, device=DEV)
+    tab = torch.tensor([X.data_ptr()], dtype=torch.int64, device=DEV)
+    ref = X.T @ X
+    assert _lib.query("ekcg_tune", 2, target) == 0
+    try:
+        chunks = _lib.query("ekcg_gram_chunks", n, 1, m, m)
+        for _ in range(3):
+            part = torch.empty(chunks * m * m, dtype=torch.float64, device=DEV)
+            G = torch.empty(m * m, dtype=torch.float64, device=DEV)
+            _lib.call("ekcg_gram", tab.data_ptr(), m, 1, m, X.data_ptr(), m, m, n, part.data_ptr(), None, stream())
+            _lib.call("ekcg_reduce", part.data_ptr(), chunks, m * m, G.data_ptr(), None, stream())
+            assert (G.view(m, m) - ref).abs().max().item() <= 1e-13 * ref.abs().max().item()
+    finally:
+        _lib.call("ekcg_tune", 2, 0)
 
 
 def test_gram_deterministic():
