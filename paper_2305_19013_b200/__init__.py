@@ -17,6 +17,7 @@ from .linalg import (
     trsm_right_inv,
 )
 from .partition import Partition, contiguous_partition, read_partition, write_partition
+from .aortho import a_cholqr, a_orthogonalize_against, pre_cholqr
 from .operators import CsrOperator, StencilOperator
 from .solvers import (
     METHODS,
@@ -61,6 +62,9 @@ __all__ = [
     "contiguous_partition",
     "read_partition",
     "write_partition",
+    "a_orthogonalize_against",
+    "a_cholqr",
+    "pre_cholqr",
     "CsrOperator",
     "StencilOperator",
     "METHODS",
