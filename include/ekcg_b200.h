@@ -165,8 +165,9 @@ int ekcg_cholesky(const double* B, int m, double tol, double* R, double* info, v
 /* ---- fused iteration kernels (m in {8,16,32,64}) -------------------------
  * Each reduces its split-K partials in-kernel (last CTA to arrive, fixed
  * order) and runs the m x m factor / bookkeeping there.  `partials` holds
- * ekcg_fused_partials(n, m) doubles; `counter` is a device uint32 that must be
- * 0 before the first call (the kernels leave it 0). */
+ * ekcg_fused_partials(n, m) doubles; `counter` points to EKCG_FUSED_COUNTERS
+ * device uint32 that must be 0 before the first call (the kernels leave them 0). */
+#define EKCG_FUSED_COUNTERS 64
 int ekcg_fused_partials(long long n, int m);
 
 /* Wout = Win - sum_i Q_i C_i (CGS2 pass 2, aortho.py:93-94) fused with

@@ -264,6 +264,22 @@ __device__ inline bool last_cta_arrive(unsigned int* counter) {
     return is_last;
 }
 
+// Like last_cta_arrive for `expected` arrivals on `counter` (a group of CTAs);
+// the last one gets true and resets the counter.
+__device__ inline bool last_arrive(unsigned int* counter, unsigned expected) {
+    __shared__ bool is_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        unsigned prev = atomicAdd(counter, 1u);
+        is_last = (prev == expected - 1);
+        if (is_last) *counter = 0u;
+    }
+    __syncthreads();
+    if (is_last) __threadfence();
+    return is_last;
+}
+
 // out[j] = sum_{p < P} partials[p*len + j] (fixed order, L2-coherent loads), by one CTA.
 __device__ inline void cta_sum_partials(const double* partials, int P, int len, double* out) {
     const int nthr = blockDim.x * blockDim.y;

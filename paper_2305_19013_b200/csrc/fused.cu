@@ -426,7 +426,7 @@ int launch_stencil_cholinv(const EkcgStencil& s, const UniformFaces& uf, long lo
 // ---------------------------------------------------------------------------
 extern "C" int ekcg_fused_partials(long long n, int m) {
     (void)n;
-    return kFusedCtas * (m * m > 1 ? m * m : 1);
+    return (kFusedCtas + 64) * (m * m > 1 ? m * m : 1);  // + group sums of the two-level reduction
 }
 
 extern "C" int ekcg_update_prechol(const double* const* Qs, int ldq, int d, const double* C, const double* Win,

@@ -307,6 +307,7 @@ int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, 
 //             the last CTA finishes the iteration (or stores |r|^2).
 // ---------------------------------------------------------------------------
 constexpr int EPI_GRAM = 1, EPI_XR = 2;
+constexpr int kRedGroup = 16;  // CTAs per first-level group of the in-kernel Gram reduction
 
 struct FusedArgs {
     double* partials;
@@ -412,12 +413,13 @@ stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil
                 double* ty = tileY + nd * KC + 4 * ig;
                 *reinterpret_cast<double2*>(ty + ha) = make_double2(o[0], o[1]);
                 *reinterpret_cast<double2*>(ty + hb) = make_double2(o[2], o[3]);
-                __syncthreads();
-                // G += X^T (A X) over the 64 nodes: 16 k-steps, two per warp; lane (i, k) reads
-                // columns 2i, 2i+1 of node k (interleaved tiles t: column 2i + t)
+                __syncwarp();
+                // G += X^T (A X) over the warp's own 8 nodes (two k-steps, no CTA barrier:
+                // warp w wrote tileY rows 8w..8w+7); lane (i, k) reads columns 2i, 2i+1 of
+                // node k (interleaved tiles t: column 2i + t)
 #pragma unroll
                 for (int h = 0; h < 2; ++h) {
-                    const int node = 4 * (warp + 8 * h) + lr;
+                    const int node = 8 * warp + 4 * h + lr;
                     const int hx = node % P::TX, hy = node / P::TX;
                     const double2 a = *reinterpret_cast<const double2*>(
                         pc + ((hy + P::OY) * P::PX + hx + 1) * KC + 2 * lc);
@@ -480,12 +482,24 @@ stencil_march_fused_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil
             for (int w = 1; w < 8; ++w) v += red[w * 256 + tid];
             fa.partials[(long long)blockIdx.x * 256 + tid] = v;
         }
-        if (last_cta_arrive(fa.counter)) {
-            double* Gm = smem + 8 * 256;
-            cta_sum_partials_mlp(fa.partials, gridDim.x, 256, Gm);
-            if (fa.finalize) cholinv_body(Gm, Gm + 256, Gm + 512, 16, fa.out, fa.ctrl, fa.iteration, fa.tol);
-            else
-                for (int e = tid; e < 256; e += 256) fa.out[e] = Gm[e];
+        // two-level fixed-order reduction: the last CTA of each group of kRedGroup
+        // consecutive CTAs sums the group's partials (one round of loads), the
+        // last group to finish sums the group sums -- instead of one CTA reading
+        // every partial (counter[1 + g]: group g, counter[0]: groups done)
+        const int ngroups = (int)((gridDim.x + kRedGroup - 1) / kRedGroup);
+        const int g = (int)(blockIdx.x / kRedGroup);
+        const int p0 = g * kRedGroup, p1 = min((int)gridDim.x, p0 + kRedGroup);
+        if (last_arrive(fa.counter + 1 + g, (unsigned)(p1 - p0))) {
+            double v = __ldcg(fa.partials + (long long)p0 * 256 + tid);
+            for (int p = p0 + 1; p < p1; ++p) v += __ldcg(fa.partials + (long long)p * 256 + tid);
+            fa.partials[((long long)gridDim.x + g) * 256 + tid] = v;
+            if (last_arrive(fa.counter, (unsigned)ngroups)) {
+                double* Gm = smem + 8 * 256;
+                cta_sum_partials_mlp(fa.partials + (long long)gridDim.x * 256, ngroups, 256, Gm);
+                if (fa.finalize) cholinv_body(Gm, Gm + 256, Gm + 512, 16, fa.out, fa.ctrl, fa.iteration, fa.tol);
+                else
+                    for (int e = tid; e < 256; e += 256) fa.out[e] = Gm[e];
+            }
         }
     } else {
         __shared__ double wsum[8];

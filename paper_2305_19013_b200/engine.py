@@ -171,7 +171,7 @@ class DeviceEngine:
         self.switch_iteration = None
         self.gram_chunks = {}
         self.launch_k = []
-        self.counter = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.counter = torch.zeros(64, dtype=torch.int32, device=dev)  # EKCG_FUSED_COUNTERS
         from .operators import StencilOperator
         self.fused_ok = isinstance(self.op, StencilOperator) and not self.no_fuse
         self.fused_part = _lib.query("ekcg_fused_partials", n, mm)

@@ -19,7 +19,7 @@ x = torch.zeros(n, dtype=torch.float64, device=dev)
 r = torch.randn(n, dtype=torch.float64, device=dev)
 alpha = torch.randn(m, dtype=torch.float64, device=dev) * 1e-3
 part = torch.empty(_lib.query("ekcg_fused_partials", n, m), dtype=torch.float64, device=dev)
-cnt = torch.zeros(1, dtype=torch.int32, device=dev)
+cnt = torch.zeros(64, dtype=torch.int32, device=dev)
 ctrl = torch.zeros(_lib.query("ekcg_ctrl_bytes"), dtype=torch.uint8, device=dev)
 ctrl[0] = 1
 G = torch.empty(m * m, dtype=torch.float64, device=dev)
