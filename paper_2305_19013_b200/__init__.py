@@ -18,6 +18,7 @@ from .linalg import (
 )
 from .partition import Partition, contiguous_partition, read_partition, write_partition
 from .aortho import a_cholqr, a_orthogonalize_against, pre_cholqr
+from .cg import cg
 from .operators import CsrOperator, StencilOperator
 from .solvers import (
     METHODS,
@@ -73,6 +74,7 @@ __all__ = [
     "ConvergenceReport",
     "BasisStore",
     "enlarged_solve",
+    "cg",
     "diffusion_csr",
     "gen_poisson2d",
     "gen_poisson3d",

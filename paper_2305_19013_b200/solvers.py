@@ -225,9 +225,9 @@ def enlarged_solve(A, b, x0=None, partition=None, cfg=None, x_star=None, on_iter
     from .engine import DeviceEngine
 
     cfg = cfg if cfg is not None else SolverConfig()
-    if cfg.method == "cg":
-        raise NotImplementedError("classical CG is outside this package's hot path; "
-                                  "use method='sre-cg2' with t=1 for the CG-equivalent enlarged solve")
+    if cfg.method == "cg":  # solvers.py:271-272
+        from .cg import cg
+        return cg(A, b, x0=x0, cfg=cfg, x_star=x_star, device=device)
     if partition is None:
         raise ValueError("enlarged methods need a partition")
     cfg.validate(partition)
