@@ -37,7 +37,7 @@ from .precond import (
     forward_solve,
     uniform_block_bounds,
 )
-from .reporting import CSV_COLUMNS, make_rhs, run_batch, write_history, write_runs_csv
+from .reporting import CSV_COLUMNS, make_rhs, run_batch, run_experiment, write_history, write_runs_csv
 from .problems import (
     box_partition,
     diffusion_csr,
@@ -84,6 +84,7 @@ __all__ = [
     "make_config",
     "make_rhs",
     "run_batch",
+    "run_experiment",
     "write_history",
     "write_runs_csv",
     "CSV_COLUMNS",
