@@ -21,6 +21,7 @@ after the second Gram-Schmidt pass has consumed it.
 
 from __future__ import annotations
 
+import os
 import time
 
 import numpy as np
@@ -124,6 +125,8 @@ class DeviceEngine:
         self.use_graphs = False
         self._capturing = False
         self._slab, self._slab_off = None, 0
+        # NVTX ranges per iteration and per tagged launch (host cost only when on)
+        self.nvtx = os.environ.get("EKCG_NVTX", "0") == "1"
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -272,10 +275,24 @@ class DeviceEngine:
         self._timed(tag, lambda: self.op.apply(x_ptr, ldx, y_ptr, ldy, m, gate, self.stream))
 
     def _timed(self, tag, fn):
+        if self.nvtx:
+            torch.cuda.nvtx.range_push(tag)
         if self.kernel_timer is None:
             fn()
         else:
             self.kernel_timer(tag, fn)
+        if self.nvtx:
+            torch.cuda.nvtx.range_pop()
+
+    def _enqueue(self, k, tol1):
+        """One iteration's launches, inside an NVTX range when EKCG_NVTX=1 (nsys timelines)."""
+        if not self.nvtx:
+            return self._enqueue_iteration(k, tol1)
+        torch.cuda.nvtx.range_push(f"iteration {k}")
+        try:
+            return self._enqueue_iteration(k, tol1)
+        finally:
+            torch.cuda.nvtx.range_pop()
 
     # -------------------------------------------------------------- store
     def _new_block(self, width):
@@ -697,7 +714,7 @@ class DeviceEngine:
         self._graphs = graphs
         while k <= self.kmax:
             if sync_each:
-                self._enqueue_iteration(k, tol1)
+                self._enqueue(k, tol1)
                 ctrl = self._read_ctrl()
                 if ctrl["k_done"] == k:
                     rho = ctrl["last_rho"]
@@ -726,7 +743,7 @@ class DeviceEngine:
                             self._host_step(k)
                         g.replay()
                     else:
-                        self._enqueue_iteration(k, 1.0)
+                        self._enqueue(k, 1.0)
                     k += 1
                 snaps.append(self._snapshot(len(snaps)))
                 if len(snaps) >= 2:
