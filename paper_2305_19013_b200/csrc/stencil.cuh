@@ -18,6 +18,13 @@ __device__ __forceinline__ double harmonic_face(double c, double klo, double khi
     return mul_rn(c, h);
 }
 
+// a / b for the tile edges: a shift when b is a power of two (every tile field
+// here; the test is uniform across the launch), else the integer division.
+__device__ __forceinline__ unsigned tile_div(unsigned a, int b) {
+    const unsigned ub = (unsigned)b;
+    return (ub & (ub - 1)) == 0 ? (a >> (__ffs(b) - 1)) : a / ub;
+}
+
 // Per-launch constants for a uniform-kappa grid (computed by the host with the
 // same IEEE operations as harmonic_face, so the same bits).
 struct UniformFaces {
@@ -65,7 +72,7 @@ __device__ __forceinline__ unsigned stencil_coef(const EkcgStencil& s, const Uni
         if (x == 0)      diag = add_rn(diag, uf.bx);
         if (x == nx - 1) diag = add_rn(diag, uf.bx);
     } else {
-        const unsigned txi = x / (unsigned)s.tx, tyi = y / (unsigned)s.ty, tzi = z / (unsigned)s.tz;
+        const unsigned txi = tile_div(x, s.tx), tyi = tile_div(y, s.ty), tzi = tile_div(z, s.tz);
         const unsigned rx = x - txi * s.tx, ry = y - tyi * s.ty, rz = z - tzi * s.tz;
         const long long fx = s.fx, fxy = (long long)s.fx * s.fy;
         const double* __restrict__ F = s.kfield;
@@ -130,7 +137,7 @@ __device__ __forceinline__ int stencil_row(const EkcgStencil& s, const UniformFa
     } else {
         // tile coordinates of the node; a neighbour lies in the adjacent tile
         // exactly when the step crosses a tile edge
-        const unsigned txi = x / (unsigned)s.tx, tyi = y / (unsigned)s.ty, tzi = z / (unsigned)s.tz;
+        const unsigned txi = tile_div(x, s.tx), tyi = tile_div(y, s.ty), tzi = tile_div(z, s.tz);
         const unsigned rx = x - txi * s.tx, ry = y - tyi * s.ty, rz = z - tzi * s.tz;
         const long long fx = s.fx, fxy = (long long)s.fx * s.fy;
         const double* __restrict__ F = s.kfield;
