@@ -47,6 +47,13 @@ typedef struct EkcgStencil {
     double kconst;
     long long row_begin, row_end;
     const double* kself;
+    /* optional, tile fields only: face coefficients between tile t and its +x /
+     * +y / +z neighbour tile, c_axis * (2 k_t k_u / (k_t + k_u)) evaluated on the
+     * host with the operations of generators.py:45 (so cross-tile faces take a
+     * load instead of a division; bitwise the same values). */
+    const double* hx;
+    const double* hy;
+    const double* hz;
 } EkcgStencil;
 
 /* ---- sparse operator and T^t split ------------------------------------ */

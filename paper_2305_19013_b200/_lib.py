@@ -74,6 +74,7 @@ class EkcgStencil(ctypes.Structure):
         ("kconst", c_double),
         ("row_begin", c_longlong), ("row_end", c_longlong),
         ("kself", c_void_p),
+        ("hx", c_void_p), ("hy", c_void_p), ("hz", c_void_p),
     ]
 
 

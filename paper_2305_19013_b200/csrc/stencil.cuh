@@ -38,13 +38,15 @@ struct UniformFaces {
 // no per-tile self-harmonic table is given); harmonic_face(c, k, k) equals
 // c * kself[tile] bitwise (same IEEE operations, evaluated on the host).
 __device__ __forceinline__ double face_lo(const EkcgStencil& s, double c, const double* F, long long tc, double kc,
-                                         bool cross, long long off) {
+                                         bool cross, long long off, const double* hcross) {
     if (!cross && s.kself != nullptr) return mul_rn(c, __ldg(s.kself + tc));
+    if (cross && hcross != nullptr) return __ldg(hcross + tc - off);  // host-built, same IEEE operations
     return harmonic_face(c, __ldg(F + tc - (cross ? off : 0)), kc);
 }
 __device__ __forceinline__ double face_hi(const EkcgStencil& s, double c, const double* F, long long tc, double kc,
-                                         bool cross, long long off) {
+                                         bool cross, long long off, const double* hcross) {
     if (!cross && s.kself != nullptr) return mul_rn(c, __ldg(s.kself + tc));
+    if (cross && hcross != nullptr) return __ldg(hcross + tc);
     return harmonic_face(c, kc, __ldg(F + tc + (cross ? off : 0)));
 }
 
@@ -79,17 +81,17 @@ __device__ __forceinline__ unsigned stencil_coef(const EkcgStencil& s, const Uni
         const long long tc = tzi * fxy + tyi * fx + txi;
         const double kc = __ldg(F + tc);
         if (three) {
-            if (z < nz - 1) { fzh = face_hi(s, s.cz, F, tc, kc, rz + 1 == (unsigned)s.tz, fxy); diag = add_rn(diag, fzh); }
-            if (z > 0)      { fzl = face_lo(s, s.cz, F, tc, kc, rz == 0, fxy); diag = add_rn(diag, fzl); }
+            if (z < nz - 1) { fzh = face_hi(s, s.cz, F, tc, kc, rz + 1 == (unsigned)s.tz, fxy, s.hz); diag = add_rn(diag, fzh); }
+            if (z > 0)      { fzl = face_lo(s, s.cz, F, tc, kc, rz == 0, fxy, s.hz); diag = add_rn(diag, fzl); }
             if (z == 0)      diag = add_rn(diag, mul_rn(s.cz, kc));
             if (z == nz - 1) diag = add_rn(diag, mul_rn(s.cz, kc));
         }
-        if (y < ny - 1) { fyh = face_hi(s, s.cy, F, tc, kc, ry + 1 == (unsigned)s.ty, fx); diag = add_rn(diag, fyh); }
-        if (y > 0)      { fyl = face_lo(s, s.cy, F, tc, kc, ry == 0, fx); diag = add_rn(diag, fyl); }
+        if (y < ny - 1) { fyh = face_hi(s, s.cy, F, tc, kc, ry + 1 == (unsigned)s.ty, fx, s.hy); diag = add_rn(diag, fyh); }
+        if (y > 0)      { fyl = face_lo(s, s.cy, F, tc, kc, ry == 0, fx, s.hy); diag = add_rn(diag, fyl); }
         if (y == 0)      diag = add_rn(diag, mul_rn(s.cy, kc));
         if (y == ny - 1) diag = add_rn(diag, mul_rn(s.cy, kc));
-        if (x < nx - 1) { fxh = face_hi(s, s.cx, F, tc, kc, rx + 1 == (unsigned)s.tx, 1); diag = add_rn(diag, fxh); }
-        if (x > 0)      { fxl = face_lo(s, s.cx, F, tc, kc, rx == 0, 1); diag = add_rn(diag, fxl); }
+        if (x < nx - 1) { fxh = face_hi(s, s.cx, F, tc, kc, rx + 1 == (unsigned)s.tx, 1, s.hx); diag = add_rn(diag, fxh); }
+        if (x > 0)      { fxl = face_lo(s, s.cx, F, tc, kc, rx == 0, 1, s.hx); diag = add_rn(diag, fxl); }
         if (x == 0)      diag = add_rn(diag, mul_rn(s.cx, kc));
         if (x == nx - 1) diag = add_rn(diag, mul_rn(s.cx, kc));
     }
@@ -144,17 +146,17 @@ __device__ __forceinline__ int stencil_row(const EkcgStencil& s, const UniformFa
         const long long tc = tzi * fxy + tyi * fx + txi;
         const double kc = __ldg(F + tc);
         if (three) {
-            if (z < nz - 1) { fzh = face_hi(s, s.cz, F, tc, kc, rz + 1 == (unsigned)s.tz, fxy); diag = add_rn(diag, fzh); }
-            if (z > 0)      { fzl = face_lo(s, s.cz, F, tc, kc, rz == 0, fxy); diag = add_rn(diag, fzl); }
+            if (z < nz - 1) { fzh = face_hi(s, s.cz, F, tc, kc, rz + 1 == (unsigned)s.tz, fxy, s.hz); diag = add_rn(diag, fzh); }
+            if (z > 0)      { fzl = face_lo(s, s.cz, F, tc, kc, rz == 0, fxy, s.hz); diag = add_rn(diag, fzl); }
             if (z == 0)      diag = add_rn(diag, mul_rn(s.cz, kc));
             if (z == nz - 1) diag = add_rn(diag, mul_rn(s.cz, kc));
         }
-        if (y < ny - 1) { fyh = face_hi(s, s.cy, F, tc, kc, ry + 1 == (unsigned)s.ty, fx); diag = add_rn(diag, fyh); }
-        if (y > 0)      { fyl = face_lo(s, s.cy, F, tc, kc, ry == 0, fx); diag = add_rn(diag, fyl); }
+        if (y < ny - 1) { fyh = face_hi(s, s.cy, F, tc, kc, ry + 1 == (unsigned)s.ty, fx, s.hy); diag = add_rn(diag, fyh); }
+        if (y > 0)      { fyl = face_lo(s, s.cy, F, tc, kc, ry == 0, fx, s.hy); diag = add_rn(diag, fyl); }
         if (y == 0)      diag = add_rn(diag, mul_rn(s.cy, kc));
         if (y == ny - 1) diag = add_rn(diag, mul_rn(s.cy, kc));
-        if (x < nx - 1) { fxh = face_hi(s, s.cx, F, tc, kc, rx + 1 == (unsigned)s.tx, 1); diag = add_rn(diag, fxh); }
-        if (x > 0)      { fxl = face_lo(s, s.cx, F, tc, kc, rx == 0, 1); diag = add_rn(diag, fxl); }
+        if (x < nx - 1) { fxh = face_hi(s, s.cx, F, tc, kc, rx + 1 == (unsigned)s.tx, 1, s.hx); diag = add_rn(diag, fxh); }
+        if (x > 0)      { fxl = face_lo(s, s.cx, F, tc, kc, rx == 0, 1, s.hx); diag = add_rn(diag, fxl); }
         if (x == 0)      diag = add_rn(diag, mul_rn(s.cx, kc));
         if (x == nx - 1) diag = add_rn(diag, mul_rn(s.cx, kc));
     }

@@ -106,6 +106,21 @@ class StencilOperator:
             self.kself = torch.from_numpy(np.ascontiguousarray(2.0 * field * field / (field + field)).reshape(-1)).to(
                 self.device)
             desc.kself = self.kself.data_ptr()
+            # faces between a tile and its +x / +y / +z neighbour tile (generators.py:45 on the
+            # host: c * ((2 k_lo k_hi) / (k_lo + k_hi)), left to right): cross-tile faces load
+            # them instead of dividing on the device
+            f3 = field if self.dim == 3 else field[None]
+            cz = coef[2] if self.dim == 3 else 1.0
+            self.hcross = []
+            for axis, c in ((2, coef[0]), (1, coef[1]), (0, cz)):
+                h = np.zeros_like(f3)
+                lo = [slice(None)] * 3
+                hi = [slice(None)] * 3
+                lo[axis], hi[axis] = slice(0, -1), slice(1, None)
+                klo, khi = f3[tuple(lo)], f3[tuple(hi)]
+                h[tuple(lo)] = c * (2.0 * klo * khi / (klo + khi))
+                self.hcross.append(torch.from_numpy(np.ascontiguousarray(h).reshape(-1)).to(self.device))
+            desc.hx, desc.hy, desc.hz = (t.data_ptr() for t in self.hcross)
             desc.tx, desc.ty = tile[0], tile[1]
             desc.tz = tile[2] if self.dim == 3 else 1
             desc.fx, desc.fy = need[0], need[1]
