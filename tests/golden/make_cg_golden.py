@@ -28,6 +28,9 @@ CASES = {
     "p3d8_pcg_ichol0_kmax": {"gen": ["poisson3d", 8, 8, 8], "xstar": "rhs:5", "kw": {"kmax": 6},
                              "precond": ["ichol0", 4], "x0": "normal:9"},
 }
+# an indefinite matrix with a positive diagonal: CG stops on nonpositive curvature
+INDEFINITE = {"n": 3, "rows": [0, 0, 1, 1, 2, 1, 2], "cols": [0, 1, 0, 1, 2, 2, 1],
+              "vals": [1.0, 2.0, 2.0, 1.0, 1.0, 0.5, 0.5], "b": [1.0, 0.0, 1.0]}
 BATCH = {"matrix": "poisson2d:10,10", "methods": ["cg", "sre-cg2"], "t": [2], "retention": ["full"],
          "precond": "bj-chol:4", "precond_mode": "modified", "tol": 1e-8, "seed": 7}
 
@@ -61,6 +64,11 @@ if __name__ == "__main__":
                               "history": [float(v) for v in rep.residual_history],
                               "true_residual": rep.true_residual, "relative_error": rep.relative_error,
                               "notes": rep.notes}
+    d = INDEFINITE
+    A = ekcg.SparseSpdMatrix.from_coo(d["n"], np.array(d["rows"]), np.array(d["cols"]), np.array(d["vals"]))
+    _, rep = ekcg.cg(A, np.array(d["b"]))
+    out["indefinite"] = {"input": d, "status": rep.status, "iterations": rep.iterations, "notes": rep.notes,
+                         "history": [float(v) for v in rep.residual_history]}
     with tempfile.TemporaryDirectory() as tmp:
         run_experiment(BATCH, tmp, render_figures=False)
         out["batch"] = {"spec": BATCH, "csv": (Path(tmp) / "runs.csv").read_text(),

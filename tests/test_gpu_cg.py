@@ -91,3 +91,15 @@ def test_preconditioned_batch_matches_reference(tmp_path):
         n = min(len(ha), len(hb), 21)
         keep = hb[:n] / hb[0] > 1e-6  # preconditioned runs reach round-off within ~15 iterations
         assert np.max(np.abs(ha[:n][keep] / ha[0] - hb[:n][keep] / hb[0]) / (hb[:n][keep] / hb[0])) <= 1e-8
+
+
+def test_cg_breakdown_on_nonpositive_curvature():
+    """An indefinite matrix (positive diagonal) stops CG with the reference's status and note."""
+    ref = GOLDEN["indefinite"]
+    d = ref["input"]
+    A = pk.SparseSpdMatrix.from_coo(d["n"], np.array(d["rows"]), np.array(d["cols"]), np.array(d["vals"]))
+    _, rep = pk.cg(A, np.array(d["b"]))
+    assert rep.status == ref["status"] == "breakdown"
+    assert rep.iterations == ref["iterations"]
+    assert rep.notes == ref["notes"]
+    np.testing.assert_allclose(rep.residual_history, ref["history"], rtol=1e-12)
