@@ -879,7 +879,7 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_tri_skip = (int)value;
         return EKCG_OK;
     }
-    if (key == 17 && value >= 0 && value <= 2) {
+    if (key == 17 && value >= 0 && value <= 3) {
         g_csr_vec = (int)value;
         return EKCG_OK;
     }

@@ -16,7 +16,18 @@
 // per row (one per column group) and R rows per block, grid-striding over
 // rows -- no 64-bit integer division in the index math.
 // ---------------------------------------------------------------------------
-int g_csr_vec = 1;  // ekcg_tune key 17: vectorized CSR SpMM (0: one thread per (row, column), 2: at most 2 columns per thread)
+int g_csr_vec = 3;  // ekcg_tune key 17: CSR SpMM kernel choice (3: software-pipelined for m = 16 / 32 / 64 / 128,
+                    // else 1; 1: vectorized; 2: at most 2 columns per thread; 0: one thread per (row, column))
+
+static int sm_count() {
+    static int sms = 0;
+    if (sms == 0) {
+        int dev = 0;
+        sms = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return sms;
+}
 
 struct RowLaunch {
     dim3 grid, block;
@@ -192,7 +203,7 @@ csr_spmm_vec_kernel(const long long* __restrict__ rp, const int* __restrict__ ci
                 cq[q] = q <= cnt ? __ldg(ci + lo + q) : 0;
                 aq[q] = q <= cnt ? __ldg(vv + lo + q) : 0.0;
             }
-            double xq[8][VEC];
+            double xq[8][VEC] = {};  // defined on every path: keeps the gathers in registers
 #pragma unroll
             for (int q = 0; q < 8; ++q) {
                 if (q <= cnt) load_xvec<VEC>(X, (long long)cq[q] * ldx + c0, xq[q]);
@@ -223,6 +234,108 @@ csr_spmm_vec_kernel(const long long* __restrict__ rp, const int* __restrict__ ci
             for (int h = 0; h < VEC / 2; ++h)
                 reinterpret_cast<double2*>(Y + i * ldy + c0)[h] = make_double2(y[2 * h], y[2 * h + 1]);
         }
+    }
+}
+
+// Software-pipelined form of csr_spmm_vec_kernel<4> for m >= 16 (G = m / 4 >= 4
+// threads per row), persistent grid.  A row costs three dependent memory
+// latencies (row pointers -> (col, value) pairs -> X gathers); here, while the
+// gathers of row i are in flight, the thread group already holds the pairs of
+// its next row and loads the row pointers of the one after, so a row costs
+// about one.  The group keeps the next row's pairs distributed (entry q in
+// thread q % G, slot q / G) and shuffles them in when the row becomes current.
+// Same products and association as csr_spmm_vec_kernel (bitwise equal).
+__global__ void __launch_bounds__(256, 2)
+csr_spmm_pf_kernel(const long long* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vv,
+                   const double* __restrict__ X, int ldx, double* __restrict__ Y, int ldy, long long n,
+                   const int* __restrict__ live) {
+    EKCG_GATE(live);
+    const int G = blockDim.x, g = threadIdx.x;
+    const int c0 = g * 4;
+    const int lane = (threadIdx.x + threadIdx.y * blockDim.x) & 31;
+    const int base = lane & ~(G - 1);  // first lane of the group (G is a power of two <= 32)
+    const long long stride = (long long)gridDim.x * blockDim.y;
+    long long i = (long long)blockIdx.x * blockDim.y + threadIdx.y;
+    long long iw = i - lane / G;  // the warp's first row: the loop is warp-uniform so shuffles see every lane
+    long long lo = 0, hi = 0, nlo = 0, nhi = 0;
+    if (i < n) {
+        lo = __ldg(rp + i);
+        hi = __ldg(rp + i + 1);
+    }
+    if (i + stride < n) {
+        nlo = __ldg(rp + i + stride);
+        nhi = __ldg(rp + i + stride + 1);
+    }
+    // this thread's share of a short row: entries g and g + G
+    auto load_share = [&](long long l, long long h, int (&c)[2], double (&a)[2]) {
+        const long long cnt = h - l - 1;
+#pragma unroll
+        for (int s = 0; s < 2; ++s) {
+            const int q = g + s * G;
+            const bool ok = h > l && cnt < 8 && q <= cnt;
+            c[s] = ok ? __ldg(ci + l + q) : 0;
+            a[s] = ok ? __ldg(vv + l + q) : 0.0;
+        }
+    };
+    int cs[2];
+    double as[2];
+    load_share(lo, hi, cs, as);
+    for (; iw < n; i += stride, iw += stride) {
+        const long long cnt = hi - lo - 1;
+        int cq[8];
+        double aq[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int s = q / G;  // uniform
+            const int src = base + (q % G);
+            cq[q] = __shfl_sync(0xffffffffu, s == 0 ? cs[0] : cs[1], src);
+            aq[q] = __shfl_sync(0xffffffffu, s == 0 ? as[0] : as[1], src);
+        }
+        double xq[8][4] = {};  // defined on every path: keeps the gathers in registers
+        if (hi > lo && cnt < 8) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+                if (q <= cnt) load_xvec<4>(X, (long long)cq[q] * ldx + c0, xq[q]);
+        }
+        // next row's pairs and the row pointers of the one after
+        load_share(nlo, nhi, cs, as);
+        long long plo = 0, phi = 0;
+        if (i + 2 * stride < n) {
+            plo = __ldg(rp + i + 2 * stride);
+            phi = __ldg(rp + i + 2 * stride + 1);
+        }
+        double y[4];
+        if (hi <= lo) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) y[v] = 0.0;
+        } else if (cnt < 8) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const double p0 = mul_rn(aq[0], xq[0][v]);
+                if (cnt == 0) {
+                    y[v] = p0;
+                } else {
+                    double acc = mul_rn(aq[1], xq[1][v]);
+#pragma unroll
+                    for (int q = 2; q < 8; ++q)
+                        if (q <= cnt) acc = add_rn(acc, mul_rn(aq[q], xq[q][v]));
+                    y[v] = add_rn(p0, acc);
+                }
+            }
+        } else {
+            const double a0 = __ldg(vv + lo);
+            const long long x0 = (long long)__ldg(ci + lo) * ldx;
+            for (int v = 0; v < 4; ++v)
+                y[v] = add_rn(mul_rn(a0, __ldg(X + x0 + c0 + v)), tail_pairwise(ci, vv, lo + 1, cnt, X, ldx, c0 + v));
+        }
+        if (i < n) {
+            reinterpret_cast<double2*>(Y + i * ldy + c0)[0] = make_double2(y[0], y[1]);
+            reinterpret_cast<double2*>(Y + i * ldy + c0)[1] = make_double2(y[2], y[3]);
+        }
+        lo = nlo;
+        hi = nhi;
+        nlo = plo;
+        nhi = phi;
     }
 }
 
@@ -304,7 +417,20 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
     cudaStream_t st = as_stream(stream);
     const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0 &&
                       ldx % 2 == 0 && ldy % 2 == 0;
-    if (g_csr_vec == 1 && m % 4 == 0 && m / 4 <= 256 && al16) {
+    const int G = m / 4;
+    if (g_csr_vec == 3 && m % 4 == 0 && (G == 4 || G == 8 || G == 16 || G == 32) && al16) {
+        static int occ = 0;
+        if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, csr_spmm_pf_kernel, 256, 0) !=
+                             cudaSuccess || occ < 1)) {
+            cudaGetLastError();
+            occ = 1;
+        }
+        const int rows = 256 / G;
+        long long blocks = (n + rows - 1) / rows, cap = (long long)occ * sm_count();
+        if (blocks > cap) blocks = cap;
+        launch_k(csr_spmm_pf_kernel, dim3((unsigned)blocks), dim3(G, rows), 0, st, row_ptr, col_idx, values, X, ldx,
+                 Y, ldy, n, live);
+    } else if (g_csr_vec && g_csr_vec != 2 && m % 4 == 0 && m / 4 <= 256 && al16) {
         RowLaunch L = row_launch(n, m / 4);
         launch_k(csr_spmm_vec_kernel<4>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
     } else if (g_csr_vec && m % 2 == 0 && m / 2 <= 256 && al16) {

@@ -70,17 +70,46 @@ def test_csr_vectorized_equals_scalar_kernel(m):
     X = dev(rng.standard_normal((n, m)))
     rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
     outs = []
-    for vec in (1, 2, 0):
+    for vec in (1, 2, 0, 3):
         _lib.call("ekcg_tune", 17, vec)
         Y = torch.empty_like(X)
         _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(), m, Y.data_ptr(),
                   m, n, m, None, stream())
         outs.append(Y.cpu().numpy())
-    _lib.call("ekcg_tune", 17, 1)
+    _lib.call("ekcg_tune", 17, 3)  # back to the default
     assert np.array_equal(outs[0].view(np.int64), outs[2].view(np.int64))
     assert np.array_equal(outs[1].view(np.int64), outs[2].view(np.int64))
+    assert np.array_equal(outs[3].view(np.int64), outs[2].view(np.int64))
     ref = orc.csr_spmm(rp, ci.astype(np.int64), vals, X.cpu().numpy())
     assert np.array_equal(outs[0].view(np.int64), ref.view(np.int64))
+
+
+@pytest.mark.parametrize("m", [16, 32, 64, 128])
+def test_csr_pipelined_equals_vectorized(m):
+    """The software-pipelined CSR kernel (ekcg_tune 17 = 3) against the vectorized
+    one, bitwise, with enough rows that every thread walks several rows (the
+    pipelined pairs / row pointers), rows of 1..20 entries and a ragged last warp."""
+    rng = np.random.default_rng(100 + m)
+    n = 300_001 if m <= 32 else 100_003
+    lens = rng.integers(1, 21, n)
+    lens[rng.random(n) < 0.7] = 7
+    rp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    ci = rng.integers(0, n, rp[-1]).astype(np.int32)
+    vals = rng.standard_normal(rp[-1])
+    X = dev(rng.standard_normal((n, m)))
+    rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
+    outs = []
+    for vec in (3, 1):
+        _lib.call("ekcg_tune", 17, vec)
+        Y = torch.full_like(X, float("nan"))
+        _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(), m, Y.data_ptr(),
+                  m, n, m, None, stream())
+        outs.append(Y.cpu().numpy())
+    _lib.call("ekcg_tune", 17, 3)  # back to the default
+    assert np.array_equal(outs[0].view(np.int64), outs[1].view(np.int64))
+    rows = np.arange(0, n, 997)
+    sub = orc.csr_spmm(rp, ci.astype(np.int64), vals, X.cpu().numpy())[rows]
+    assert np.array_equal(outs[0][rows].view(np.int64), sub.view(np.int64))
 
 
 @pytest.mark.parametrize("idx,edge", [(1, 20), (2, 8), (3, 16), (4, 8), (5, 64)])

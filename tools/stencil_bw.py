@@ -57,11 +57,11 @@ for c in (int(v) for v in args.configs.split(",")):
             from paper_2305_19013_b200.operators import CsrOperator
             A = prob.csr()
             cop = CsrOperator(A, "cuda")
-            for vec in (1, 2, 0):
+            for vec in (3, 1, 2, 0):
                 _lib.call("ekcg_tune", 17, vec)
                 ms, _ = bw(cop, m, args.reps)
                 nbytes = 16.0 * op.n * m + 12.0 * A.nnz + 8.0 * (op.n + 1)
                 print(json.dumps({"config": c, "m": m, "csr_vec": vec, "csr_ms": ms,
                                   "csr_GBs": round(nbytes / (ms / 1e3) / 1e9, 1)}), flush=True)
-            _lib.call("ekcg_tune", 17, 1)
+            _lib.call("ekcg_tune", 17, 3)
             del cop, A
