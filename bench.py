@@ -22,6 +22,7 @@ import subprocess
 import sys
 import threading
 import time
+import types
 from pathlib import Path
 
 import numpy as np
@@ -342,15 +343,22 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         b_host = torch.from_numpy(np.ascontiguousarray(prob.b)).pin_memory()
+        # The reference-facing call: the host CSR matrix a reference user holds (SparseSpdMatrix layout),
+        # host b in, host x out -- the matrix upload, the operator set-up and the D2H are all timed.
+        # A plain (n, row_ptr, col_idx, values) object like the reference's SparseSpdMatrix, so nothing is
+        # cached on the device between calls: every call uploads the matrix.
+        csr = prob.csr()
+        A_host = types.SimpleNamespace(n=csr.n, row_ptr=csr.row_ptr, col_idx=csr.col_idx, values=csr.values)
+        mat_bytes = 8 * (csr.n + 1) + 12 * csr.nnz
         # one untimed warm-up call of the public API path (first-call host costs)
-        pk.enlarged_solve(op, b_host.numpy(), partition=prob.partition, cfg=cfg, device=dev)
+        pk.enlarged_solve(A_host, b_host.numpy(), partition=prob.partition, cfg=cfg, device=dev)
         e2e_ms, e2e_it = [], 0
         for _ in range(max(1, args.steps)):
             flush.fill_(1.0)
             barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
-            x, rep = pk.enlarged_solve(op, b_host.numpy(), partition=prob.partition, cfg=cfg, device=dev)
+            x, rep = pk.enlarged_solve(A_host, b_host.numpy(), partition=prob.partition, cfg=cfg, device=dev)
             e1.record()
             e1.synchronize()
             e2e_ms.append(e0.elapsed_time(e1))
@@ -362,8 +370,9 @@ def run_ours(args):
             e2e_tot = float(t.item())
             if not sharded:
                 e2e_it *= world
-        e2e = {"value": e2e_it / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n,
-               "d2h_bytes_per_step": 8 * n + 8 * (reps[-1].iterations + 1)}
+        e2e = {"value": e2e_it / (e2e_tot / 1e3), "unit": UNIT, "h2d_bytes_per_step": 8 * n + mat_bytes,
+               "d2h_bytes_per_step": 8 * n + 8 * (reps[-1].iterations + 1),
+               "call": "enlarged_solve(host CSR matrix, host numpy b) -> host x, report"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
