@@ -41,6 +41,7 @@ int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const 
 extern int g_update_stream;
 extern int g_wide_stream;
 extern int g_csr_vec;
+extern int g_csr_w256;
 extern int g_wide_upd_variant;
 int gram_wide_slots(int gb);
 int launch_gram_wide(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
@@ -881,6 +882,10 @@ extern "C" int ekcg_tune(int key, long long value) {
     }
     if (key == 17 && value >= 0 && value <= 3) {
         g_csr_vec = (int)value;
+        return EKCG_OK;
+    }
+    if (key == 22 && (value == 0 || value == 1)) {
+        g_csr_w256 = (int)value;
         return EKCG_OK;
     }
     if (key == 21 && value >= 0 && value <= 4) {

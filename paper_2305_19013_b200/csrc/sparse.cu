@@ -19,6 +19,8 @@
 int g_csr_vec = 3;  // ekcg_tune key 17: CSR SpMM kernel choice (3: software-pipelined for m = 16 / 32 / 64 / 128,
                     // else 1; 1: vectorized; 2: at most 2 columns per thread; 0: one thread per (row, column))
 
+int g_csr_w256 = 1;  // ekcg_tune key 22: 256-bit X gathers / Y stores in the pipelined CSR kernel when 32-B aligned
+
 static int sm_count() {
     static int sms = 0;
     if (sms == 0) {
@@ -237,25 +239,72 @@ csr_spmm_vec_kernel(const long long* __restrict__ rp, const int* __restrict__ ci
     }
 }
 
-// Software-pipelined form of csr_spmm_vec_kernel<4> for m >= 16 (G = m / 4 >= 4
-// threads per row), persistent grid.  A row costs three dependent memory
+// One short row (CNT + 1 <= 8 entries) for 4 columns: all gathers issued up
+// front, then `pre` (the next row's loads), then the sum in the reference
+// association p0 + (((p1 + p2) + p3) + ...).  CNT is a template argument so the
+// gathers are unpredicated and exactly as many as the row has.
+// 4 doubles with one 256-bit access (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a; 32-B aligned)
+__device__ __forceinline__ void ld4_256(const double* p, double (&v)[4]) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st4_256(double* p, const double (&v)[4]) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
+template <int CNT, bool W256, class Pre>
+__device__ __forceinline__ void csr_short_row(const int (&cq)[8], const double (&aq)[8],
+                                              const double* __restrict__ X, int ldx, int c0, double (&y)[4],
+                                              Pre&& pre) {
+    double xq[CNT + 1][4];
+#pragma unroll
+    for (int q = 0; q <= CNT; ++q) {
+        if (W256)
+            ld4_256(X + (long long)cq[q] * ldx + c0, xq[q]);
+        else
+            load_xvec<4>(X, (long long)cq[q] * ldx + c0, xq[q]);
+    }
+    pre();
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        const double p0 = mul_rn(aq[0], xq[0][v]);
+        if (CNT == 0) {
+            y[v] = p0;
+        } else {
+            double acc = mul_rn(aq[1], xq[1][v]);
+#pragma unroll
+            for (int q = 2; q <= CNT; ++q) acc = add_rn(acc, mul_rn(aq[q], xq[q][v]));
+            y[v] = add_rn(p0, acc);
+        }
+    }
+}
+
+// Software-pipelined form of csr_spmm_vec_kernel<4> for m = 4G, G in {4, 8, 16,
+// 32} threads per row, persistent grid.  A row costs three dependent memory
 // latencies (row pointers -> (col, value) pairs -> X gathers); here, while the
 // gathers of row i are in flight, the thread group already holds the pairs of
 // its next row and loads the row pointers of the one after, so a row costs
 // about one.  The group keeps the next row's pairs distributed (entry q in
-// thread q % G, slot q / G) and shuffles them in when the row becomes current.
-// Same products and association as csr_spmm_vec_kernel (bitwise equal).
+// thread q % G, slot q / G) and shuffles them in when the row becomes current;
+// short rows dispatch on their length to an unpredicated body.  Same products
+// and association as csr_spmm_vec_kernel (bitwise equal).
+template <int G, bool W256>
 __global__ void __launch_bounds__(256, 2)
 csr_spmm_pf_kernel(const long long* __restrict__ rp, const int* __restrict__ ci, const double* __restrict__ vv,
                    const double* __restrict__ X, int ldx, double* __restrict__ Y, int ldy, long long n,
                    const int* __restrict__ live) {
+    static_assert(G == 4 || G == 8 || G == 16 || G == 32, "G is a power of two in [4, 32]");
+    constexpr int S = G >= 8 ? 1 : 2;  // slots per thread
+    constexpr int R = 256 / G;         // rows per block
     EKCG_GATE(live);
-    const int G = blockDim.x, g = threadIdx.x;
+    const int g = threadIdx.x;
     const int c0 = g * 4;
-    const int lane = (threadIdx.x + threadIdx.y * blockDim.x) & 31;
-    const int base = lane & ~(G - 1);  // first lane of the group (G is a power of two <= 32)
-    const long long stride = (long long)gridDim.x * blockDim.y;
-    long long i = (long long)blockIdx.x * blockDim.y + threadIdx.y;
+    const int lane = (threadIdx.x + threadIdx.y * G) & 31;
+    const int base = lane & ~(G - 1);  // first lane of the group
+    const long long stride = (long long)gridDim.x * R;
+    long long i = (long long)blockIdx.x * R + threadIdx.y;
     long long iw = i - lane / G;  // the warp's first row: the loop is warp-uniform so shuffles see every lane
     long long lo = 0, hi = 0, nlo = 0, nhi = 0;
     if (i < n) {
@@ -266,77 +315,91 @@ csr_spmm_pf_kernel(const long long* __restrict__ rp, const int* __restrict__ ci,
         nlo = __ldg(rp + i + stride);
         nhi = __ldg(rp + i + stride + 1);
     }
-    // this thread's share of a short row: entries g and g + G
-    auto load_share = [&](long long l, long long h, int (&c)[2], double (&a)[2]) {
+    int cs[S];
+    double as[S];
+    // this thread's share of a short row: entries g (+ G)
+    auto load_share = [&](long long l, long long h) {
         const long long cnt = h - l - 1;
 #pragma unroll
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < S; ++s) {
             const int q = g + s * G;
             const bool ok = h > l && cnt < 8 && q <= cnt;
-            c[s] = ok ? __ldg(ci + l + q) : 0;
-            a[s] = ok ? __ldg(vv + l + q) : 0.0;
+            cs[s] = ok ? __ldg(ci + l + q) : 0;
+            as[s] = ok ? __ldg(vv + l + q) : 0.0;
         }
     };
-    int cs[2];
-    double as[2];
-    load_share(lo, hi, cs, as);
+    load_share(lo, hi);
     for (; iw < n; i += stride, iw += stride) {
         const long long cnt = hi - lo - 1;
         int cq[8];
         double aq[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-            const int s = q / G;  // uniform
-            const int src = base + (q % G);
-            cq[q] = __shfl_sync(0xffffffffu, s == 0 ? cs[0] : cs[1], src);
-            aq[q] = __shfl_sync(0xffffffffu, s == 0 ? as[0] : as[1], src);
-        }
-        double xq[8][4] = {};  // defined on every path: keeps the gathers in registers
-        if (hi > lo && cnt < 8) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-                if (q <= cnt) load_xvec<4>(X, (long long)cq[q] * ldx + c0, xq[q]);
-        }
-        // next row's pairs and the row pointers of the one after
-        load_share(nlo, nhi, cs, as);
-        long long plo = 0, phi = 0;
-        if (i + 2 * stride < n) {
-            plo = __ldg(rp + i + 2 * stride);
-            phi = __ldg(rp + i + 2 * stride + 1);
-        }
-        double y[4];
-        if (hi <= lo) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) y[v] = 0.0;
-        } else if (cnt < 8) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v) {
-                const double p0 = mul_rn(aq[0], xq[0][v]);
-                if (cnt == 0) {
-                    y[v] = p0;
-                } else {
-                    double acc = mul_rn(aq[1], xq[1][v]);
-#pragma unroll
-                    for (int q = 2; q < 8; ++q)
-                        if (q <= cnt) acc = add_rn(acc, mul_rn(aq[q], xq[q][v]));
-                    y[v] = add_rn(p0, acc);
-                }
+            if (q / G < S) {
+                cq[q] = __shfl_sync(0xffffffffu, cs[q / G < S ? q / G : 0], base + (q % G));
+                aq[q] = __shfl_sync(0xffffffffu, as[q / G < S ? q / G : 0], base + (q % G));
             }
-        } else {
-            const double a0 = __ldg(vv + lo);
-            const long long x0 = (long long)__ldg(ci + lo) * ldx;
-            for (int v = 0; v < 4; ++v)
-                y[v] = add_rn(mul_rn(a0, __ldg(X + x0 + c0 + v)), tail_pairwise(ci, vv, lo + 1, cnt, X, ldx, c0 + v));
+        }
+        long long plo = 0, phi = 0;
+        auto pre = [&]() {  // next row's pairs and the row pointers of the one after
+            load_share(nlo, nhi);
+            if (i + 2 * stride < n) {
+                plo = __ldg(rp + i + 2 * stride);
+                phi = __ldg(rp + i + 2 * stride + 1);
+            }
+        };
+        double y[4];
+        switch (hi <= lo ? -1 : (cnt < 8 ? (int)cnt : 8)) {
+            case 0: csr_short_row<0, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 1: csr_short_row<1, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 2: csr_short_row<2, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 3: csr_short_row<3, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 4: csr_short_row<4, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 5: csr_short_row<5, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 6: csr_short_row<6, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 7: csr_short_row<7, W256>(cq, aq, X, ldx, c0, y, pre); break;
+            case 8: {
+                pre();
+                const double a0 = __ldg(vv + lo);
+                const long long x0 = (long long)__ldg(ci + lo) * ldx;
+                for (int v = 0; v < 4; ++v)
+                    y[v] = add_rn(mul_rn(a0, __ldg(X + x0 + c0 + v)),
+                                  tail_pairwise(ci, vv, lo + 1, cnt, X, ldx, c0 + v));
+                break;
+            }
+            default:  // empty row, or past the end
+                pre();
+#pragma unroll
+                for (int v = 0; v < 4; ++v) y[v] = 0.0;
         }
         if (i < n) {
-            reinterpret_cast<double2*>(Y + i * ldy + c0)[0] = make_double2(y[0], y[1]);
-            reinterpret_cast<double2*>(Y + i * ldy + c0)[1] = make_double2(y[2], y[3]);
+            if (W256) {
+                st4_256(Y + i * ldy + c0, y);
+            } else {
+                reinterpret_cast<double2*>(Y + i * ldy + c0)[0] = make_double2(y[0], y[1]);
+                reinterpret_cast<double2*>(Y + i * ldy + c0)[1] = make_double2(y[2], y[3]);
+            }
         }
         lo = nlo;
         hi = nhi;
         nlo = plo;
         nhi = phi;
     }
+}
+
+template <int G, bool W256>
+static void launch_csr_pf(const long long* rp, const int* ci, const double* vv, const double* X, int ldx, double* Y,
+                          int ldy, long long n, const int* live, cudaStream_t st) {
+    static int occ = 0;
+    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, csr_spmm_pf_kernel<G, W256>, 256, 0) !=
+                         cudaSuccess || occ < 1)) {
+        cudaGetLastError();
+        occ = 1;
+    }
+    constexpr int R = 256 / G;
+    long long blocks = (n + R - 1) / R, cap = (long long)occ * sm_count();
+    if (blocks > cap) blocks = cap;
+    launch_k(csr_spmm_pf_kernel<G, W256>, dim3((unsigned)blocks), dim3(G, R), 0, st, rp, ci, vv, X, ldx, Y, ldy, n, live);
 }
 
 // ---------------------------------------------------------------------------
@@ -419,17 +482,19 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
                       ldx % 2 == 0 && ldy % 2 == 0;
     const int G = m / 4;
     if (g_csr_vec == 3 && m % 4 == 0 && (G == 4 || G == 8 || G == 16 || G == 32) && al16) {
-        static int occ = 0;
-        if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, csr_spmm_pf_kernel, 256, 0) !=
-                             cudaSuccess || occ < 1)) {
-            cudaGetLastError();
-            occ = 1;
+        const bool al32 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 31) == 0 &&
+                          ldx % 4 == 0 && ldy % 4 == 0 && g_csr_w256;
+        if (al32) {
+            if (G == 4) launch_csr_pf<4, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+            else if (G == 8) launch_csr_pf<8, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+            else if (G == 16) launch_csr_pf<16, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+            else launch_csr_pf<32, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+        } else {
+            if (G == 4) launch_csr_pf<4, false>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+            else if (G == 8) launch_csr_pf<8, false>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+            else if (G == 16) launch_csr_pf<16, false>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
+            else launch_csr_pf<32, false>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
         }
-        const int rows = 256 / G;
-        long long blocks = (n + rows - 1) / rows, cap = (long long)occ * sm_count();
-        if (blocks > cap) blocks = cap;
-        launch_k(csr_spmm_pf_kernel, dim3((unsigned)blocks), dim3(G, rows), 0, st, row_ptr, col_idx, values, X, ldx,
-                 Y, ldy, n, live);
     } else if (g_csr_vec && g_csr_vec != 2 && m % 4 == 0 && m / 4 <= 256 && al16) {
         RowLaunch L = row_launch(n, m / 4);
         launch_k(csr_spmm_vec_kernel<4>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);

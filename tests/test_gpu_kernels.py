@@ -99,14 +99,17 @@ def test_csr_pipelined_equals_vectorized(m):
     X = dev(rng.standard_normal((n, m)))
     rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
     outs = []
-    for vec in (3, 1):
+    for vec, w256 in ((3, 1), (1, 1), (3, 0)):  # pipelined with 256-bit / 128-bit accesses, vectorized
         _lib.call("ekcg_tune", 17, vec)
+        _lib.call("ekcg_tune", 22, w256)
         Y = torch.full_like(X, float("nan"))
         _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(), m, Y.data_ptr(),
                   m, n, m, None, stream())
         outs.append(Y.cpu().numpy())
-    _lib.call("ekcg_tune", 17, 3)  # back to the default
+    _lib.call("ekcg_tune", 17, 3)  # back to the defaults
+    _lib.call("ekcg_tune", 22, 1)
     assert np.array_equal(outs[0].view(np.int64), outs[1].view(np.int64))
+    assert np.array_equal(outs[2].view(np.int64), outs[1].view(np.int64))
     rows = np.arange(0, n, 997)
     sub = orc.csr_spmm(rp, ci.astype(np.int64), vals, X.cpu().numpy())[rows]
     assert np.array_equal(outs[0][rows].view(np.int64), sub.view(np.int64))

@@ -1,4 +1,4 @@
-"""One CSR SpMM of a config operator for ncu: python tools/prof_csr.py config m"""
+"""One CSR SpMM of a config operator for ncu: python tools/prof_csr.py config m [kernel choice, ekcg_tune 17]"""
 import sys
 
 import torch
@@ -8,6 +8,9 @@ from paper_2305_19013_b200.operators import CsrOperator  # noqa: E402
 from paper_2305_19013_b200.problems import make_config  # noqa: E402
 
 c, m = int(sys.argv[1]), int(sys.argv[2])
+if len(sys.argv) > 3:
+    from paper_2305_19013_b200 import _lib  # noqa: E402
+    _lib.call("ekcg_tune", 17, int(sys.argv[3]))
 prob = make_config(c, device_rhs=False)
 op = CsrOperator(prob.csr(), "cuda")
 X = torch.randn(prob.n * m, dtype=torch.float64, device="cuda")

@@ -57,11 +57,12 @@ for c in (int(v) for v in args.configs.split(",")):
             from paper_2305_19013_b200.operators import CsrOperator
             A = prob.csr()
             cop = CsrOperator(A, "cuda")
-            for vec in (3, 1, 2, 0):
+            for vec, w256 in ((3, 1), (3, 0), (1, 1), (2, 1), (0, 1)):
                 _lib.call("ekcg_tune", 17, vec)
+                _lib.call("ekcg_tune", 22, w256)
                 ms, _ = bw(cop, m, args.reps)
                 nbytes = 16.0 * op.n * m + 12.0 * A.nnz + 8.0 * (op.n + 1)
-                print(json.dumps({"config": c, "m": m, "csr_vec": vec, "csr_ms": ms,
+                print(json.dumps({"config": c, "m": m, "csr_vec": vec, "w256": w256, "csr_ms": ms,
                                   "csr_GBs": round(nbytes / (ms / 1e3) / 1e9, 1)}), flush=True)
             _lib.call("ekcg_tune", 17, 3)
             del cop, A
