@@ -74,6 +74,17 @@ __device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(
 // Fragment ownership (lane = threadIdx.x % 32):
 //   A: row lane>>2, col lane&3;   B: row (k) lane&3, col (n) lane>>2;
 //   C: row lane>>2, cols 2*(lane&3) + {0,1}.
+// 4 doubles with one 256-bit access (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a; 32-B aligned)
+__device__ __forceinline__ void ld4_256(const double* p, double (&v)[4]) {
+    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+}
+__device__ __forceinline__ void st4_256(double* p, const double (&v)[4]) {
+    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+                 : "memory");
+}
+
 __device__ __forceinline__ void dmma_8x8x4(double (&acc)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(acc[0]), "+d"(acc[1])

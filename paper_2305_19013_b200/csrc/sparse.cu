@@ -243,17 +243,6 @@ csr_spmm_vec_kernel(const long long* __restrict__ rp, const int* __restrict__ ci
 // front, then `pre` (the next row's loads), then the sum in the reference
 // association p0 + (((p1 + p2) + p3) + ...).  CNT is a template argument so the
 // gathers are unpredicated and exactly as many as the row has.
-// 4 doubles with one 256-bit access (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a; 32-B aligned)
-__device__ __forceinline__ void ld4_256(const double* p, double (&v)[4]) {
-    asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
-                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
-                 : "l"(p));
-}
-__device__ __forceinline__ void st4_256(double* p, const double (&v)[4]) {
-    asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
-                 : "memory");
-}
-
 template <int CNT, bool W256, class Pre>
 __device__ __forceinline__ void csr_short_row(const int (&cq)[8], const double (&aq)[8],
                                               const double* __restrict__ X, int ldx, int c0, double (&y)[4],
