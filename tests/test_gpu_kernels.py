@@ -115,6 +115,29 @@ def test_csr_pipelined_equals_vectorized(m):
     assert np.array_equal(outs[0][rows].view(np.int64), sub.view(np.int64))
 
 
+
+@pytest.mark.parametrize("shift", [0, 2, 1])
+def test_csr_offset_blocks(shift):
+    """X and Y blocks starting `shift` doubles into their buffers (32-B aligned, 16-B only, 8-B only): the
+    dispatch falls back from the 256-bit to the 128-bit to the scalar kernel, all bitwise equal to the oracle."""
+    rng = np.random.default_rng(7 + shift)
+    n, m = 20_011, 16
+    lens = rng.integers(1, 12, n)
+    rp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    ci = rng.integers(0, n, rp[-1]).astype(np.int32)
+    vals = rng.standard_normal(rp[-1])
+    Xh = rng.standard_normal((n, m))
+    Xbuf = torch.zeros(n * m + 8, dtype=torch.float64, device="cuda")
+    Xbuf[shift:shift + n * m] = dev(Xh).reshape(-1)
+    Ybuf = torch.full((n * m + 8,), float("nan"), dtype=torch.float64, device="cuda")
+    rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
+    _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), Xbuf.data_ptr() + 8 * shift, m,
+              Ybuf.data_ptr() + 8 * shift, m, n, m, None, stream())
+    Y = Ybuf[shift:shift + n * m].reshape(n, m).cpu().numpy()
+    ref = orc.csr_spmm(rp, ci.astype(np.int64), vals, Xh)
+    assert np.array_equal(Y.view(np.int64), ref.view(np.int64))
+
+
 @pytest.mark.parametrize("idx,edge", [(1, 20), (2, 8), (3, 16), (4, 8), (5, 64)])
 @pytest.mark.parametrize("m", [1, 2, 7, 16, 32])
 def test_stencil_equals_csr_bitwise(idx, edge, m):
