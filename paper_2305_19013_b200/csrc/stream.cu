@@ -321,7 +321,7 @@ int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const do
     }
 }
 
-int g_update_stream = 2;  // ekcg_tune key 8: streamed update for 16-column blocks, 0 off, 1.. variants
+int g_update_stream = 5;  // ekcg_tune key 8: streamed update for 16-column blocks, 0 off, 1.. variants
 
 int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
                          double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,

@@ -62,7 +62,7 @@ def sweep(m, shape, d):
         u = timeit(lambda: _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m,
                                      W.data_ptr(), m, m, 1.0, -1.0, n, None, st))
         out[f"update_s{us}"] = dict(s=u, GBs=8 * (d + 2) * n * m / u / 1e9, TF=2 * d * m * m * n / u / 1e12)
-    _lib.call("ekcg_tune", 8, 2)
+    _lib.call("ekcg_tune", 8, 5)
     _lib.call("ekcg_tune", 15, 1)
     _lib.call("ekcg_tune", 16, 0)
     op = StencilOperator(shape, 1.0)

@@ -18,14 +18,17 @@ def dram_bytes(rep):
     for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
         i = hdr.index(k)
         tot += float(vals[i]) * scale[units[i]]
-    return int(tot)
+    return int(tot), vals[hdr.index("Kernel Name")].split("(")[0]
 
 
-out = {}
+out, names = {}, []
 for tag, rep, nblk in (("hist_gram", "prof_hist_gram", D + 1), ("hist_update", "prof_hist_update", D + 2)):
     p = ROOT / "gpurun_out" / f"{rep}.ncu-rep"
-    out[tag] = dram_bytes(p)
+    out[tag], name = dram_bytes(p)
+    names.append(name.replace("void ", "").replace("<unnamed>::", ""))
     out[tag + "_alg"] = 8 * N * M * nblk
     out[tag + "_d"] = D
+out["source"] = (f"ncu --set full --clock-control none, {names[0]} / {names[1]} at d={D} "
+                 "(profiles/r01_prof_hist_*.ncu-rep)")
 (ROOT / "profiles" / "r01_traffic.json").write_text(json.dumps(out) + "\n")
 print(out)
