@@ -21,6 +21,7 @@ after the second Gram-Schmidt pass has consumed it.
 
 from __future__ import annotations
 
+import math
 import os
 import time
 
@@ -95,6 +96,9 @@ class DeviceEngine:
         self.stag_window = max(20, self.kmax // 10) if self.retention == "restart" else 0
         self.sync_mode = False
         self.max_lookahead = 16
+        # size run-ahead batches from the residual decay seen in the snapshots, so that
+        # few gated (no-op) iterations are queued past convergence
+        self.predict_batches = True
         self.kernel_timer = None  # optional hook: (name, callable) -> runs callable
         self.no_fuse = False      # force the unfused kernel sequence (tests / A-B timing)
         # fused stages in use when the operator/width allow: "prechol" (update2 + Graw + S0),
@@ -684,8 +688,28 @@ class DeviceEngine:
     def _wait_snapshot(self, snap):
         buf, ev = snap
         ev.synchronize()
-        ints = buf.numpy()[:32].view(np.int32)
-        return {"live": int(ints[0]), "status": int(ints[1]), "k_done": int(ints[2])}
+        raw = buf.numpy()
+        ints = raw[:32].view(np.int32)
+        dbl = raw[32:80].view(np.float64)
+        return {"live": int(ints[0]), "status": int(ints[1]), "k_done": int(ints[2]),
+                "tol_abs": float(dbl[3]), "last_rho": float(dbl[5])}
+
+    @staticmethod
+    def _batch_size(lookahead, seen, k_next):
+        """Iterations to queue next: the doubling look-ahead, cut to what the residual
+        decay between the last two snapshots predicts is still needed (x1.25 + 2), so
+        that few gated no-op iterations sit in the queue past convergence.  Never 0;
+        a low prediction only costs an extra poll.  Identical on every row shard
+        (the snapshots hold allreduced values)."""
+        if len(seen) < 2:
+            return lookahead
+        (k0, r0), (k1, r1) = ((c["k_done"], c["last_rho"]) for c in seen[-2:])
+        tol_abs = seen[-1]["tol_abs"]
+        if k1 <= k0 or not (0.0 < r1 < r0) or not tol_abs > 0.0:
+            return lookahead
+        left = math.log(tol_abs / r1) / math.log(r1 / r0) * (k1 - k0) if r1 > tol_abs else 0.0
+        need = math.ceil(1.25 * left) + 2 - ((k_next - 1) - k1)
+        return max(1, min(lookahead, need))
 
     # ---------------------------------------------------------------- solve
     def solve(self, b, x0=None, x_star=None, on_iteration=None):
@@ -706,7 +730,8 @@ class DeviceEngine:
             c = self._read_ctrl()
             host_hist = [c["rho0"]]
         k = 1
-        lookahead = 1
+        lookahead = batch = 1
+        seen = []
         tol1 = 1.0
         ctrl = None
         snaps = []
@@ -729,7 +754,7 @@ class DeviceEngine:
                 # run ahead: snapshot the control block after every batch and
                 # only wait for the PREVIOUS batch's snapshot, so the GPU queue
                 # never drains while the host polls
-                for _ in range(lookahead):
+                for _ in range(batch):
                     if k > self.kmax:
                         break
                     w = self.window
@@ -750,7 +775,9 @@ class DeviceEngine:
                     prev = self._wait_snapshot(snaps[-2])
                     if prev["live"] == 0:
                         break
+                    seen.append(prev)
                 lookahead = min(2 * lookahead, self.max_lookahead)
+                batch = self._batch_size(lookahead, seen, k) if self.predict_batches else lookahead
         ctrl = self._read_ctrl()  # after a full sync: the final state
         ev1.record()
         ev1.synchronize()
