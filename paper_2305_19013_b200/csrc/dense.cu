@@ -56,6 +56,7 @@ int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu
 int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
 long long g_march_min_work = 1LL << 21;
 int g_pdl = 1;  // programmatic dependent launch on (ekcg_tune key 14)
+int g_vec256 = 1;  // ekcg_tune key 24: 256-bit row loads in the x/r update and X^T y when 32-B aligned
 int g_tri_skip = 1;  // ekcg_tune key 18: ekcg_tri_apply skips the zero blocks of S (m = 64)
 int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
 int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
@@ -358,7 +359,7 @@ gram_generic_kernel(const double* const* __restrict__ Xs, int ldx, int m1, const
 // LN lanes per row, 4 columns per lane, U row groups in flight per warp; the
 // CTA's warps are combined in fixed order into its partial (same layout as
 // the Gram kernels).
-template <int LN, int U>
+template <int LN, int U, bool W256 = false>
 __global__ void __launch_bounds__(256)
 gemvt4_kernel(const double* const* __restrict__ Xs, int ldx, int d, const double* __restrict__ y, long long n,
               long long rows_chunk, double* __restrict__ partials, const int* __restrict__ live) {
@@ -372,6 +373,8 @@ gemvt4_kernel(const double* const* __restrict__ Xs, int ldx, int d, const double
     const long long r0 = blockIdx.x * rows_chunk;
     const long long r1 = min(n, r0 + rows_chunk);
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    // one 256-bit access per row segment when the block is 32-B aligned (block-uniform branch)
+    const bool w256 = W256 && ((reinterpret_cast<uintptr_t>(X) & 31) == 0) && (ldx & 3) == 0;
     for (long long base = r0 + (long long)warp * RPW * U; base < r1; base += 8LL * RPW * U) {
         double2 a[U][2];
         double yv[U];
@@ -380,8 +383,15 @@ gemvt4_kernel(const double* const* __restrict__ Xs, int ldx, int d, const double
             const long long r = base + u * RPW + sub;
             const bool ok = r < r1;
             const double2* row = reinterpret_cast<const double2*>(X + r * ldx) + 2 * li;
-            a[u][0] = ok ? __ldg(row) : make_double2(0.0, 0.0);
-            a[u][1] = ok ? __ldg(row + 1) : make_double2(0.0, 0.0);
+            if (w256) {
+                double t4[4] = {0.0, 0.0, 0.0, 0.0};
+                if (ok) ld4_256(reinterpret_cast<const double*>(row), t4);
+                a[u][0] = make_double2(t4[0], t4[1]);
+                a[u][1] = make_double2(t4[2], t4[3]);
+            } else {
+                a[u][0] = ok ? __ldg(row) : make_double2(0.0, 0.0);
+                a[u][1] = ok ? __ldg(row + 1) : make_double2(0.0, 0.0);
+            }
             yv[u] = ok ? __ldg(y + r) : 0.0;
         }
 #pragma unroll
@@ -708,7 +718,7 @@ xr_update_kernel(const double* __restrict__ W, int ldw, const double* __restrict
 
 // m = 4*LN columns, 16-B aligned rows: LN lanes per row, 4 columns per lane,
 // U row groups in flight per warp (x and r loaded before the reductions).
-template <int LN, int U>
+template <int LN, int U, bool W256 = false>
 __global__ void __launch_bounds__(kVecThreads)
 xr_update4_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ AW, int ldaw,
                   const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ r, long long n,
@@ -731,7 +741,21 @@ xr_update4_kernel(const double* __restrict__ W, int ldw, const double* __restric
             if (row < n) {
                 const double2* w = reinterpret_cast<const double2*>(W + row * ldw) + 2 * li;
                 const double2* aw = reinterpret_cast<const double2*>(AW + row * ldaw) + 2 * li;
-                const double2 w0 = __ldg(w), w1 = __ldg(w + 1), v0 = __ldg(aw), v1 = __ldg(aw + 1);
+                double2 w0, w1, v0, v1;
+                if (W256) {  // one 256-bit access per operand (32-B aligned rows)
+                    double t4[4], u4[4];
+                    ld4_256(reinterpret_cast<const double*>(w), t4);
+                    ld4_256(reinterpret_cast<const double*>(aw), u4);
+                    w0 = make_double2(t4[0], t4[1]);
+                    w1 = make_double2(t4[2], t4[3]);
+                    v0 = make_double2(u4[0], u4[1]);
+                    v1 = make_double2(u4[2], u4[3]);
+                } else {
+                    w0 = __ldg(w);
+                    w1 = __ldg(w + 1);
+                    v0 = __ldg(aw);
+                    v1 = __ldg(aw + 1);
+                }
                 if (li == 0) {
                     xv[u] = x[row];
                     rv[u] = r[row];
@@ -884,6 +908,10 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_csr_vec = (int)value;
         return EKCG_OK;
     }
+    if (key == 24 && (value == 0 || value == 1)) {
+        g_vec256 = (int)value;
+        return EKCG_OK;
+    }
     if (key == 22 && (value == 0 || value == 1)) {
         g_csr_w256 = (int)value;
         return EKCG_OK;
@@ -962,12 +990,12 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     if (vec4) {
         const dim3 g(chunks, d);
         switch (m1) {
-            case 4: launch_k(gemvt4_kernel<1, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 8: launch_k(gemvt4_kernel<2, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 16: launch_k(gemvt4_kernel<4, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 32: launch_k(gemvt4_kernel<8, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 64: launch_k(gemvt4_kernel<16, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            default: launch_k(gemvt4_kernel<32, 2>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 4: launch_k(g_vec256 ? gemvt4_kernel<1, 4, true> : gemvt4_kernel<1, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 8: launch_k(g_vec256 ? gemvt4_kernel<2, 4, true> : gemvt4_kernel<2, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 16: launch_k(g_vec256 ? gemvt4_kernel<4, 4, true> : gemvt4_kernel<4, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 32: launch_k(g_vec256 ? gemvt4_kernel<8, 4, true> : gemvt4_kernel<8, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 64: launch_k(g_vec256 ? gemvt4_kernel<16, 4, true> : gemvt4_kernel<16, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            default: launch_k(g_vec256 ? gemvt4_kernel<32, 2, true> : gemvt4_kernel<32, 2>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
         }
     } else if (fn != nullptr && launch_gram_wide(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, gb, partials, live, st) == EKCG_OK) {
         // streamed (TMA bulk) Gram for 32-column blocks, stream_wide.cu
@@ -1075,9 +1103,15 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
     cudaStream_t st = as_stream(stream);
     const int g = vec_chunks(n);
 #define XR_LAUNCH(L) launch_k(xr_update_kernel<L>, g, kVecThreads, 0, st, W, ldw, AW, ldaw, alpha, m, x, r, n, rho2_partials, live)
-#define XR4_LAUNCH(LN) launch_k(xr_update4_kernel<LN, 4>, g, kVecThreads, 0, st, W, ldw, AW, ldaw, alpha, x, r, n, rho2_partials, live)
+#define XR4_LAUNCH(LN)                                                                                         \
+    (al32 ? launch_k(xr_update4_kernel<LN, 4, true>, g, kVecThreads, 0, st, W, ldw, AW, ldaw, alpha, x, r, n,   \
+                     rho2_partials, live)                                                                         \
+          : launch_k(xr_update4_kernel<LN, 4>, g, kVecThreads, 0, st, W, ldw, AW, ldaw, alpha, x, r, n,         \
+                     rho2_partials, live))
     const bool al = (ldw % 2 == 0) && (ldaw % 2 == 0) && ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(AW) |
                                                            reinterpret_cast<uintptr_t>(alpha)) % 16 == 0);
+    const bool al32 = g_vec256 && ldw % 4 == 0 && ldaw % 4 == 0 &&
+                      ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(AW)) % 32 == 0);
     if (al && m == 64) XR4_LAUNCH(16);
     else if (al && m == 32) XR4_LAUNCH(8);
     else if (al && m == 16) XR4_LAUNCH(4);

@@ -262,6 +262,36 @@ def test_gram_multi_block(m1, m2, n):
         assert (got[i] - ref).abs().max().item() <= 1e-13 * scale
 
 
+@pytest.mark.parametrize("m", [4, 8, 16, 32, 64])
+def test_vec256_paths_bitwise(m):
+    """X^T y (m2 = 1) and the fused x / r update with 256-bit row loads (ekcg_tune 24) against the
+    128-bit loads: the same products and sums, so bitwise equal; plus a tolerance check on X^T y."""
+    rng = np.random.default_rng(240 + m)
+    n, d = 300_007, 2
+    Xs = [dev(rng.standard_normal((n, m))) for _ in range(d)]
+    y = dev(rng.standard_normal(n))
+    tab = torch.tensor([x.data_ptr() for x in Xs], dtype=torch.int64, device=DEV)
+    chunks = _lib.query("ekcg_gram_chunks", n, d, m, 1)
+    part = torch.empty(chunks * d * m, dtype=torch.float64, device=DEV)
+    alpha = dev(rng.standard_normal(m) * 1e-2)
+    vchunks = _lib.query("ekcg_vec_chunks", n)
+    outs = {}
+    for v in (1, 0):
+        _lib.call("ekcg_tune", 24, v)
+        g = torch.empty(d * m, dtype=torch.float64, device=DEV)
+        _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, y.data_ptr(), 1, 1, n, part.data_ptr(), None, stream())
+        _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m, g.data_ptr(), None, stream())
+        x, r = dev(rng.standard_normal(n) * 0 + 1.0), y.clone()
+        vp = torch.empty(vchunks, dtype=torch.float64, device=DEV)
+        _lib.call("ekcg_xr_update", Xs[0].data_ptr(), m, Xs[1].data_ptr(), m, alpha.data_ptr(), m, x.data_ptr(),
+                  r.data_ptr(), n, vp.data_ptr(), None, stream())
+        outs[v] = [t.cpu().numpy() for t in (g, x, r, vp)]
+    _lib.call("ekcg_tune", 24, 1)
+    for a, b in zip(outs[1], outs[0]):
+        assert np.array_equal(a.view(np.int64), b.view(np.int64))
+    ref = torch.stack([X.T @ y for X in Xs]).reshape(-1).cpu().numpy()
+    assert np.max(np.abs(outs[1][0] - ref)) <= 1e-12 * np.max(np.abs(ref))
+
 @pytest.mark.parametrize("n", [37, 4099, 200_000])
 @pytest.mark.parametrize("m", [16, 64])
 def test_gram_self_symmetric_shortcut(n, m):
