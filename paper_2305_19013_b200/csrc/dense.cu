@@ -285,7 +285,7 @@ int gram_chunks(long long n, int d, int m1, int m2) {
         // count whose CTA total fills its last wave best (equal work per CTA),
         // preferring fewer chunks; at least 1024 rows per chunk.
         const bool d1 = !wide && d == 1 && g_gram16_d1;  // GB = 1 stream kernel: 3 CTAs per SM
-        const long long slots = wide ? gram_wide_slots(gb) : d1 ? 3 * 148 : 148;
+        const long long slots = wide ? gram_wide_slots(gb) : d1 ? 3 * 148 : (g_gram_stream >= 9 ? 2 * 148 : 148);
         long long pmax = (n + (d1 ? 511 : 1023)) / (d1 ? 512 : 1024);
         const long long cap = (4 * slots + groups - 1) / groups;
         if (pmax > cap) pmax = cap;
@@ -948,7 +948,7 @@ extern "C" int ekcg_tune(int key, long long value) {
         g_update_stream = (int)value;
         return EKCG_OK;
     }
-    if (key == 7 && value >= 0 && value <= 8) {
+    if (key == 7 && value >= 0 && value <= 10) {
         g_gram_stream = (int)value;
         return EKCG_OK;
     }

@@ -299,7 +299,7 @@ int launch_update16_stream(const double* const* Qs, int d, const double* C, cons
 
 }  // namespace
 
-int g_gram_stream = 3;  // ekcg_tune key 7: streamed Gram for 16-column blocks, 0 off, 1.. variants
+int g_gram_stream = 10;  // ekcg_tune key 7: streamed Gram for 16-column blocks, 0 off, 1.. variants
 int g_gram16_d1 = 1;    // ekcg_tune key 21: one-block (d = 1) streamed Gram with GB = 1 (3 CTAs per SM)
 
 // Streamed Gram when it applies (16 contiguous columns, aligned); EKCG_EINVAL otherwise.
@@ -317,6 +317,8 @@ int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const do
         case 6: return launch_gram16_stream<2, 128, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
         case 7: return launch_gram16_stream<8, 32, 5>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
         case 8: return launch_gram16_stream<4, 48, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
+        case 9: return launch_gram16_stream<4, 32, 5>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
+        case 10: return launch_gram16_stream<4, 48, 3>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
         default: return launch_gram16_stream<4, 32, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
     }
 }

@@ -50,14 +50,14 @@ for d in ds:
            "reduce_us": round(tr * 1e6, 1), "chunks": ch,
            "update_us": round(tu * 1e6, 1), "update_frac": round(bu / tu / HBM, 3)}
     if "--variants" in sys.argv:
-        for v in range(1, 9):
+        for v in range(1, 11):
             _lib.call("ekcg_tune", 7, v)
             chv = _lib.query("ekcg_gram_chunks", n, d, m, m)
             pv = torch.empty(max(chv * d * m * m, 1 << 16), dtype=torch.float64, device=dev)
             t = timeit(lambda: _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Y.data_ptr(), m, m, n, pv.data_ptr(),
                                          None, st))
             row[f"g{v}"] = round(bg / t / HBM, 3)
-        _lib.call("ekcg_tune", 7, 3)
+        _lib.call("ekcg_tune", 7, 10)
         for v in range(1, 8):
             _lib.call("ekcg_tune", 8, v)
             t = timeit(lambda: _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), Y.data_ptr(), m,

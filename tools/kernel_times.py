@@ -50,7 +50,7 @@ def sweep(m, shape, d):
             g = timeit(lambda: _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Y.data_ptr(), m, m, n, part.data_ptr(),
                                          None, st))
             out[f"gram_s{gs}_t{tgt}"] = dict(s=g, GBs=8 * (d + 1) * n * m / g / 1e9, TF=2 * d * m * m * n / g / 1e12)
-    _lib.call("ekcg_tune", 7, 3)
+    _lib.call("ekcg_tune", 7, 10)
     _lib.call("ekcg_tune", 2, 0)
     _lib.call("ekcg_tune", 5, -1)
     for us in ((0, 2, 5, 6, 7) if m == 16 else (0, 10, 11, 12)):
