@@ -319,3 +319,146 @@ def run_oracle(row_ptr, col_idx, values, b, owner, t, *, method="sre-cg2", s=1,
     if x_star is not None:
         out["relative_error"] = float(np.linalg.norm(x - x_star) / np.linalg.norm(x_star))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Bounded-memory restatement for the full-size fixtures of configs 4 and 5
+# (tests/golden/make_full_golden.py).  Same sequence as run_oracle, with
+#  * the sparse product done in row chunks (reduceat segments are per row, so
+#    every row's association -- and every output bit -- is unchanged);
+#  * A Q_i recomputed from Q_i when the projection needs it instead of cached
+#    (the cached block IS op(Q_i), aortho.py:110, so the bits are the same);
+#  * in-place / row-chunked forms of the block updates, column scaling and
+#    triangular solves (row-independent operations).
+# Only the BLAS Gram products keep their whole-block form.  The test
+# tests/test_oracle_golden.py::test_lowmem_oracle_matches checks it against
+# run_oracle on small problems with many chunks.
+# ---------------------------------------------------------------------------
+
+def csr_spmm_chunked(row_ptr, col_idx, values, X, chunk_rows, out=None):
+    """csr_spmm / csr_spmv over row chunks (bitwise the same as the unchunked forms)."""
+    n = row_ptr.shape[0] - 1
+    vec = X.ndim == 1
+    Y = out if out is not None else np.empty(X.shape)
+    for a in range(0, n, chunk_rows):
+        b = min(n, a + chunk_rows)
+        lo, hi = int(row_ptr[a]), int(row_ptr[b])
+        rp = row_ptr[a:b + 1] - lo
+        if vec:
+            Y[a:b] = csr_spmv(rp, col_idx[lo:hi], values[lo:hi], X)
+        else:
+            m = X.shape[1]
+            scale = values[lo:hi, None]
+            ci = col_idx[lo:hi]
+            for c0 in range(0, m, COLUMN_SLAB):
+                c1 = min(m, c0 + COLUMN_SLAB)
+                Y[a:b, c0:c1] = np.add.reduceat(scale * X[ci, c0:c1], rp[:-1], axis=0)
+    return Y
+
+
+def _colnorms_chunked(W, chunk_rows):
+    """np.linalg.norm(W, axis=0) without an n x m temporary: the axis-0 reduction
+    of a C-ordered block accumulates row after row, so carrying the running sum
+    across chunks keeps the association."""
+    acc = None
+    for a in range(0, W.shape[0], chunk_rows):
+        sq = W[a:a + chunk_rows] * W[a:a + chunk_rows]
+        acc = np.add.reduce(sq if acc is None else np.vstack([acc[None, :], sq]), axis=0)
+    return np.sqrt(acc)
+
+
+def _tri_solve_inplace(W, R, chunk_rows):
+    """W <- W R^-1 row chunk by row chunk (each row solves its own system)."""
+    if np.any(np.diag(R) == 0.0):
+        raise np.linalg.LinAlgError("singular triangular factor")
+    for a in range(0, W.shape[0], chunk_rows):
+        W[a:a + chunk_rows] = solve_triangular(R, W[a:a + chunk_rows].T, trans="T", lower=False).T
+
+
+def run_oracle_lowmem(row_ptr, col_idx, values, b, owner, t, *, method="sre-cg2", s=1, tol=1e-8, kmax=None,
+                      retention="trunc", trunc=None, true_residual_every=50, chunk_rows=1 << 18,
+                      on_iteration=None):
+    """run_oracle for unpreconditioned SRE-CG2 / SRE-CG (s >= 1, full or truncated
+    retention) holding only the retained Q blocks, the candidate and one scratch
+    block: what lets the config-4 (256^3, n x 64) fixture run on a 62 GB host."""
+    if method not in ("sre-cg2", "sre-cg") or retention not in ("trunc", "full"):
+        raise ValueError("run_oracle_lowmem covers sre-cg2 / sre-cg with trunc or full retention")
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    col_idx = np.asarray(col_idx, dtype=np.int64)
+    values = np.asarray(values, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    owner = np.asarray(owner, dtype=np.int64)
+    n = b.shape[0]
+    cr = int(chunk_rows)
+    op = lambda X, out=None: csr_spmm_chunked(row_ptr, col_idx, values, X, cr, out)  # noqa: E731
+    window = 2 if method == "sre-cg" else (trunc if retention == "trunc" else None)
+    kmax = kmax if kmax is not None else 2 * n
+
+    x = np.zeros(n)
+    r = b - op(x)
+    rho0 = float(np.linalg.norm(r))
+    history = [rho0]
+    Qs = []  # retained Q blocks (A Q recomputed on use)
+    cols, peak = 0, 0
+    true_checks, notes = [], []
+    status = "converged" if rho0 == 0.0 else None
+    prev_aw_tail = None  # newest t columns of A W_{k-1}: the next candidate's first slab
+    k = 1
+    while status is None and history[-1] > tol * rho0 and k <= kmax:
+        m = s * t
+        W = np.empty((n, m))
+        if not Qs:
+            W[:, :t] = split_block(owner, t, r)
+        else:
+            W[:, :t] = prev_aw_tail
+        for i in range(1, s):  # s-step chain (run_oracle.build_chain)
+            W[:, i * t:(i + 1) * t] = op(np.ascontiguousarray(W[:, (i - 1) * t:i * t]))
+        prev_aw_tail = None
+        try:
+            for _ in range(2):  # cgs2_project: all coefficients from the same W
+                coeffs = []
+                for q in Qs:
+                    aq = op(q)
+                    coeffs.append(aq.T @ W)
+                    del aq
+                for q, c in zip(Qs, coeffs):
+                    for a in range(0, n, cr):
+                        W[a:a + cr] -= q[a:a + cr] @ c
+            # pre_cholqr_block (aortho.py:98-110)
+            norms = _colnorms_chunked(W, cr)
+            if np.any(norms == 0.0):
+                raise OracleBreakdown(f"zero column {int(np.argmin(norms))} entering Pre-CholQR")
+            for a in range(0, n, cr):
+                W[a:a + cr] /= norms
+            _tri_solve_inplace(W, small_cholesky(symmetrize(W.T @ W)), cr)
+            AW = op(W)
+            _tri_solve_inplace(W, small_cholesky(symmetrize(W.T @ AW)), cr)
+            op(W, out=AW)
+        except OracleBreakdown as exc:
+            status = "breakdown"
+            notes.append(f"basis breakdown at iteration {k}: {exc}")
+            break
+        Qs.append(W)
+        cols += m
+        peak = max(peak, cols)
+        while window is not None and len(Qs) > window:
+            Qs.pop(0)
+            cols -= m
+        alpha = W.T @ r
+        x = x + W @ alpha
+        r = r - AW @ alpha
+        prev_aw_tail = AW if s == 1 else AW[:, m - t:].copy()
+        del AW
+        rho = float(np.linalg.norm(r))
+        tol1 = abs(rho - history[-1]) / rho0
+        history.append(rho)
+        if k % true_residual_every == 0:
+            true_checks.append((k, float(np.linalg.norm(b - op(x)))))
+        if on_iteration is not None:
+            on_iteration({"k": k, "rho": rho, "tol1": tol1})
+        k += 1
+    if status is None:
+        status = "converged" if history[-1] <= tol * rho0 else "maxiter"
+    return {"status": status, "iterations": len(history) - 1, "residual_history": np.array(history),
+            "peak_block_vectors": peak, "true_residual_checks": true_checks, "x": x, "notes": notes,
+            "true_residual": float(np.linalg.norm(b - op(x)))}

@@ -465,7 +465,7 @@ class DeviceEngine:
                 self.S.data_ptr(), live, self._karg(k), 1e-14, 1, st))
         else:
             self._apply_op(WB, m, WC, m, m)
-            self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_self")
+            self._gram(WB_arr, m, 1, m, WC, m, m, self.G.data_ptr(), tag="gram_aw")
             _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, self._karg(k), 1e-14, st)
         if fused and "vec" in self.fuse and m <= 16:
             # W_k = W0 S + alpha = W_k^T r (for m >= 32 the smem-staged update + X^T r kernel is faster)
@@ -553,7 +553,7 @@ class DeviceEngine:
                 self.S.data_ptr(), live, self._karg(k), 1e-14, 1, st))
         else:
             self._apply_op(WC, m, WA, m, m)  # A W0 -> WA (free)
-            self._gram(WC_arr, m, 1, m, WA, m, m, self.G.data_ptr(), tag="gram_self")
+            self._gram(WC_arr, m, 1, m, WA, m, m, self.G.data_ptr(), tag="gram_aw")
             _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, self._karg(k), 1e-14, st)
         if fused and m <= 16:
             self._timed("tri_alpha", lambda: _lib.call(

@@ -241,7 +241,7 @@ class ShardedEngine(DeviceEngine):
         self._tri_apply(WA_arr, m, self.S0.data_ptr(), lWC, m, m)  # W0 -> WC
         self._exchange(self.WC, m)
         self._apply_ext(self.WC, 0, m, lWA, m, m, live)  # A W0 -> WA (free)
-        self._gram(WC_arr, m, 1, m, lWA, m, m, self.G.data_ptr(), tag="gram_self")
+        self._gram(WC_arr, m, 1, m, lWA, m, m, self.G.data_ptr(), tag="gram_aw")
         self.comm.allreduce_(self.G[: m * m])
         _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
         self._tri_apply(WC_arr, m, self.S.data_ptr(), lq(blk), m, m)
@@ -327,7 +327,7 @@ class ShardedEngine(DeviceEngine):
                       part.data_ptr(), self.counter.data_ptr(), self.G.data_ptr(), live, k, 1e-14, 0, st)
         else:
             self._apply_ext(self.WB, 0, m, self.WC.data_ptr(), m, m, live)
-            self._gram(WB_arr, m, 1, m, self.WC.data_ptr(), m, m, self.G.data_ptr(), tag="gram_self")
+            self._gram(WB_arr, m, 1, m, self.WC.data_ptr(), m, m, self.G.data_ptr(), tag="gram_aw")
         self.comm.allreduce_(self.G[: m * m])
         _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
         if fused_st:

@@ -125,3 +125,56 @@ def test_sstep_converges_in_fewer_outer_iterations(solves_golden):
     assert two["status"] == "converged"
     assert two["iterations"] <= (one["iterations"] + 1) // 2 + 2
     assert two["peak_block_vectors"] == 8 * two["iterations"]
+
+
+@pytest.mark.parametrize("idx,edge,kmax", [(4, 16, 5), (5, 64, 10), (3, 16, 8), (2, 12, 200)])
+def test_lowmem_oracle_matches(idx, edge, kmax):
+    """The bounded-memory restatement used for the full-size fixtures (row-chunked
+    products, A Q recomputed) is bitwise run_oracle, here with 37-row chunks."""
+    from paper_2305_19013_b200.problems import make_config
+    prob = make_config(idx, edge, device_rhs=False)
+    A = prob.csr()
+    kw = dict(prob.solver_kwargs, kmax=kmax)
+    t = kw.pop("t")
+    ref = orc.run_oracle(A.row_ptr, A.col_idx, A.values, prob.b, prob.partition.owner(), t, **kw)
+    low = orc.run_oracle_lowmem(A.row_ptr, A.col_idx, A.values, prob.b, prob.partition.owner(), t,
+                                chunk_rows=37, **kw)
+    assert low["status"] == ref["status"] and low["iterations"] == ref["iterations"]
+    assert np.array_equal(low["residual_history"], ref["residual_history"])
+    assert np.array_equal(low["x"], ref["x"])
+    assert low["peak_block_vectors"] == ref["peak_block_vectors"]
+
+
+def test_chunked_spmm_bitwise(kernels_golden):
+    g = kernels_golden
+    for tag in ("a", "b", "c"):
+        rp, ci, v, X = g[f"spmm_{tag}_rp"], g[f"spmm_{tag}_ci"], g[f"spmm_{tag}_v"], g[f"spmm_{tag}_X"]
+        assert np.array_equal(orc.csr_spmm_chunked(rp, ci, v, X, 7), g[f"spmm_{tag}_Y"])
+        assert np.array_equal(orc.csr_spmm_chunked(rp, ci, v, X[:, 3].copy(), 11), g[f"spmv_{tag}_y"])
+
+
+def test_full_size_fixture_inputs():
+    """The full-size fixtures (make_full_golden.py) were built from the same inputs the
+    package's generators produce: b, owner map, and (cfg3) the reference generator's CSR."""
+    import hashlib
+    import json
+    from pathlib import Path
+    from paper_2305_19013_b200.problems import make_config
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    gold = Path(__file__).resolve().parent / "golden"
+    p3 = gold / "full_cfg3.json"
+    if p3.exists():
+        fx = json.loads(p3.read_text())
+        prob = make_config(3, fx["edge"], device_rhs=False)
+        assert sha(prob.b) == fx["b_sha256"] and sha(prob.partition.owner()) == fx["owner_sha256"]
+        A = prob.csr()
+        h = hashlib.sha256()
+        for arr in (A.row_ptr.astype(np.int64), A.col_idx.astype(np.int64), A.values.astype(np.float64)):
+            h.update(np.ascontiguousarray(arr).tobytes())
+        assert h.hexdigest() == fx["csr_sha256"]
+    p5 = gold / "full_cfg5.json"
+    if p5.exists():
+        fx = json.loads(p5.read_text())
+        prob = make_config(5, fx["edge"], device_rhs=False)
+        assert sha(prob.b) == fx["b_sha256"] and sha(prob.partition.owner()) == fx["owner_sha256"]
+        assert sha(prob.kappa_field) == fx["kappa_field_sha256"]
