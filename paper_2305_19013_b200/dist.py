@@ -1,14 +1,24 @@
-"""Row sharding across GPUs: slabs of whole grid layers, neighbour
-halo exchange and small allreduces, over torch.distributed (NCCL on GPUs, gloo
-on CPU for the host-side tests).
+"""Row sharding across GPUs over torch.distributed (NCCL on GPUs,
+gloo on CPU for the host-side tests): the decompositions, the halo plans, and
+the collectives the sharded engine issues.
 
-Rows are kept in the reference's x-fastest order; rank p owns the contiguous
-rows of layers [l0, l1) of the slowest grid axis (z in 3-D, y in 2-D).  The
-T^t split is row-local (a rank may own rows of several subdomains), the
-stencil SpMM needs one layer of halo from each neighbour, and every Gram /
-norm is a sum of per-rank partials reduced with one allreduce.  NCCL hands
-every rank the same reduced bytes, so the m x m factorizations computed
-redundantly on each rank agree bit for bit.
+* Stencil operators (`RowShard`): rank p owns the contiguous rows of whole
+  grid layers [l0, l1) of the slowest axis (z in 3-D, y in 2-D), in the
+  reference's x-fastest order.  The stencil SpMM needs one layer of halo from
+  each neighbour.  DESIGN.md section 7 gives the halo volumes against box
+  decompositions; for config 5 (8 x 8 boxes) and at G = 2 for every config the
+  slabs are exactly whole t-subdomains (partition.py:14-68).
+* CSR matrices (`CsrShard`): rows renumbered subdomain-major
+  (`subdomain_order`), so rank p owns whole subdomains [p t/G, (p+1) t/G) --
+  the t-subdomain decomposition of north_star -- with each rank's interior
+  rows (no off-rank column) first.  The halo is every off-rank row the local
+  entries reference, exchanged with whichever peers own them.
+
+The T^t split is row-local either way, every Gram / norm is a sum of per-rank
+partials reduced with one allreduce, and NCCL hands every rank the same
+reduced bytes, so the m x m factorizations computed redundantly on each rank
+agree bit for bit.  Exchanges come in start / wait halves so the engine can
+run the interior rows of a product while the halo is in flight.
 """
 
 from __future__ import annotations
@@ -42,6 +52,16 @@ class RowShard:
         self.has_lo = rank > 0
         self.has_hi = rank < world - 1
 
+    def row_ranges(self):
+        """(interior, boundary) global row ranges: the interior needs no halo row, so
+        it can run while the halo is exchanged; the boundary layers run after."""
+        lo = self.row_begin + (self.plane if self.has_lo else 0)
+        hi = self.row_end - (self.plane if self.has_hi else 0)
+        if hi <= lo:
+            return None, [(self.row_begin, self.row_end)]
+        bnd = [r for r in ((self.row_begin, lo), (hi, self.row_end)) if r[1] > r[0]]
+        return (lo, hi), bnd
+
     @property
     def ext_rows(self):
         return self.n_local + 2 * self.halo
@@ -59,6 +79,52 @@ class RowShard:
 
     def __repr__(self):
         return f"RowShard(rank={self.rank}/{self.world}, rows=[{self.row_begin}, {self.row_end}), halo={self.halo})"
+
+
+def subdomain_order(owner, t, world, row_ptr=None, col_idx=None):
+    """Subdomain-major renumbering for a CSR shard (the t-subdomain decomposition).
+
+    Returns (order, bounds): new row i is old row order[i]; rank p owns new rows
+    [bounds[p], bounds[p+1]) = the whole subdomains [p t/G, (p+1) t/G).  Within a
+    rank, rows whose columns all stay on the rank (interior) come first, so one
+    contiguous range can run while the halo is in flight.  None when t % G != 0.
+    The order inside each class is ascending, like the paper's METIS renumbering
+    a symmetric permutation: the SpMM keeps every row's entries (and bits), only
+    the Gram reductions change order.
+    """
+    owner = np.asarray(owner, dtype=np.int64)
+    if world < 1 or t % world:
+        return None
+    per = t // world
+    rank_of = owner // per
+    order = np.argsort(rank_of, kind="stable")
+    counts = np.bincount(rank_of, minlength=world)
+    bounds = np.concatenate(([0], np.cumsum(counts))).astype(np.int64)
+    if row_ptr is not None:
+        row_ptr = np.asarray(row_ptr, dtype=np.int64)
+        col_rank = rank_of[np.asarray(col_idx, dtype=np.int64)]
+        row_of = np.repeat(np.arange(len(owner)), np.diff(row_ptr))
+        off = np.zeros(len(owner), dtype=bool)
+        np.logical_or.at(off, row_of, col_rank != rank_of[row_of])
+        # per rank: interior rows first, then boundary rows (both ascending)
+        key = rank_of * 2 + off.astype(np.int64)
+        order = np.argsort(key, kind="stable")
+    return order, bounds
+
+
+def permute_csr(row_ptr, col_idx, values, order):
+    """P A P^T for new row i = old row order[i]; every row keeps its entries in
+    their stored order (column ids renumbered), so each row's products and their
+    association -- hence the SpMM bits -- are the reference's."""
+    row_ptr = np.asarray(row_ptr, dtype=np.int64)
+    n = len(row_ptr) - 1
+    inv = np.empty(n, dtype=np.int64)
+    inv[order] = np.arange(n)
+    lens = np.diff(row_ptr)[order]
+    new_ptr = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    starts = row_ptr[:-1][order]
+    idx = np.repeat(starts - new_ptr[:-1], lens) + np.arange(new_ptr[-1])
+    return new_ptr, inv[np.asarray(col_idx, dtype=np.int64)[idx]], np.asarray(values, dtype=np.float64)[idx]
 
 
 def row_bounds(n, world):
@@ -100,6 +166,13 @@ class CsrShard:
                                   self.halo_lo + self.n_local + np.searchsorted(self.hi_rows, cols)))
         self.local_row_ptr = row_ptr[self.row_begin:self.row_end + 1] - e0
         self.local_col_idx = local.astype(np.int32)
+        # the longest run of local rows that reference no halo row: it runs during the exchange
+        off = (cols < self.row_begin) | (cols >= self.row_end)
+        lens = np.diff(self.local_row_ptr)
+        needs = np.zeros(self.n_local, dtype=bool)
+        if off.any():
+            needs[np.repeat(np.arange(self.n_local), lens)[off]] = True
+        self.interior = _longest_false_run(needs)
         # rows needed from each owner: contiguous ranges of the extended block
         self.recv = {}
         for rows, base in ((self.lo_rows, 0), (self.hi_rows, self.halo_lo + self.n_local)):
@@ -117,6 +190,13 @@ class CsrShard:
     def ext_rows(self):
         return self.halo_lo + self.n_local + self.halo_hi
 
+    def row_ranges(self):
+        """(interior, boundary) local row ranges (see RowShard.row_ranges)."""
+        a, b = self.interior
+        if b <= a:
+            return None, [(0, self.n_local)]
+        return (a, b), [r for r in ((0, a), (b, self.n_local)) if r[1] > r[0]]
+
     def n_local_of(self, rank):
         return int(self.bounds[rank + 1] - self.bounds[rank])
 
@@ -131,6 +211,19 @@ class CsrShard:
         self.send = {q: (np.asarray(r, dtype=np.int64) - self.row_begin) for q, r in enumerate(got)
                      if r is not None and len(r)}
         return self
+
+
+def _longest_false_run(mask):
+    """[a, b) of the longest run of False in a boolean vector ((0, 0) if none)."""
+    if mask.size == 0:
+        return 0, 0
+    x = np.concatenate(([True], mask, [True]))
+    edges = np.flatnonzero(np.diff(x.astype(np.int8)))  # run starts (True->False) and ends
+    starts, ends = edges[0::2], edges[1::2]
+    if starts.size == 0:
+        return 0, 0
+    j = int(np.argmax(ends - starts))
+    return int(starts[j]), int(ends[j])
 
 
 class Comm:
@@ -155,15 +248,26 @@ class Comm:
         return t
 
     def halo_exchange(self, ext, ld, shard):
-        """Fill the halo layers of an extended row block.
+        self.wait(self.halo_exchange_start(ext, ld, shard))
+
+    @staticmethod
+    def wait(works):
+        """Make the current stream wait for a started exchange (NCCL: a stream wait, not a host block)."""
+        for w in works or ():
+            w.wait()
+
+    def halo_exchange_start(self, ext, ld, shard):
+        """Start filling the halo layers of an extended row block; returns the works.
 
         `ext` is a flat tensor of shard.ext_rows * ld values laid out as
         [lower halo | local rows | upper halo]; the first local layer goes to
         the lower neighbour's upper halo and the last local layer to the upper
-        neighbour's lower halo.
+        neighbour's lower halo.  The sends read only the first / last local
+        layers and the receives write only the halos, so kernels on the current
+        stream that read the local rows may run while the works are in flight.
         """
         if self.world == 1:
-            return
+            return None
         h = shard.halo * ld
         nl = shard.n_local * ld
         ops = []
@@ -173,9 +277,7 @@ class Comm:
         if shard.has_hi:
             ops.append(dist.P2POp(dist.isend, ext[nl:nl + h], shard.rank + 1, self.group))
             ops.append(dist.P2POp(dist.irecv, ext[nl + h:nl + 2 * h], shard.rank + 1, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        return dist.batch_isend_irecv(ops) if ops else None
 
     def exchange_objects(self, per_rank):
         """Send per_rank[q] to rank q; return the list received from every rank."""
@@ -189,11 +291,14 @@ class Comm:
         return out
 
     def csr_exchange(self, ext, ld, shard, send_idx):
-        """Fill the halo rows of an extended block [lo | local | hi] of a CsrShard:
-        pack the rows each peer needs (send_idx[q]: device index tensors of local
-        rows) and receive each peer's rows straight into their halo range."""
+        self.wait(self.csr_exchange_start(ext, ld, shard, send_idx))
+
+    def csr_exchange_start(self, ext, ld, shard, send_idx):
+        """Start filling the halo rows of an extended block [lo | local | hi] of a
+        CsrShard: pack the rows each peer needs (send_idx[q]: device index tensors
+        of local rows) and receive each peer's rows straight into their halo range."""
         if self.world == 1:
-            return
+            return None
         E = ext[: shard.ext_rows * ld].view(shard.ext_rows, ld)
         loc = E[shard.lo:shard.lo + shard.n_local]
         ops, keep = [], []
@@ -203,9 +308,11 @@ class Comm:
             ops.append(dist.P2POp(dist.isend, buf.view(-1), q, self.group))
         for q, (start, count, _) in shard.recv.items():
             ops.append(dist.P2POp(dist.irecv, E[start:start + count].view(-1), q, self.group))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        if not ops:
+            return None
+        works = dist.batch_isend_irecv(ops)
+        self._keep = keep  # packed send buffers live until the next exchange is issued
+        return works
 
     def gather_rows(self, local, shard):
         """Concatenate every rank's local rows (uneven slabs padded for all_gather)."""

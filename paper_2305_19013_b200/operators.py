@@ -46,6 +46,15 @@ class CsrOperator:
         _lib.call("ekcg_spmm_csr", self.row_ptr.data_ptr(), self.col_idx.data_ptr(), self.values.data_ptr(),
                   _ptr(X), ldx, _ptr(Y), ldy, self.n, m, live, st)
 
+    def apply_rows(self, r0, r1, X, ldx, Y, ldy, m, live=None, stream=None):
+        """Rows [r0, r1) of Y = A X (Y points at row 0): the row pointers keep
+        addressing the full column / value arrays, so a sub-range is a pointer shift."""
+        if r1 <= r0:
+            return
+        st = current_stream_ptr(self.device) if stream is None else stream
+        _lib.call("ekcg_spmm_csr", self.row_ptr.data_ptr() + 8 * r0, self.col_idx.data_ptr(),
+                  self.values.data_ptr(), _ptr(X), ldx, _ptr(Y) + 8 * r0 * ldy, ldy, r1 - r0, m, live, st)
+
 
 class StencilOperator:
     """`_diffusion_matrix(shape, kappa)` (generators.py:25-60) applied matrix-free.

@@ -32,7 +32,8 @@ import numpy as np
 import torch
 
 from . import _lib
-from .dist import Comm, CsrShard, RowShard
+from .dist import Comm, CsrShard, RowShard, permute_csr, subdomain_order
+from .partition import Partition
 from .engine import F64, DeviceEngine, _Block
 from .operators import CsrOperator, StencilOperator
 
@@ -40,22 +41,28 @@ from .operators import CsrOperator, StencilOperator
 class _LocalCsr:
     """The local rows of a CsrShard as a CSR whose columns index the extended block."""
 
-    def __init__(self, A, shard):
-        e0, e1 = int(A.row_ptr[shard.row_begin]), int(A.row_ptr[shard.row_end])
+    def __init__(self, row_ptr, values, shard):
+        e0, e1 = int(row_ptr[shard.row_begin]), int(row_ptr[shard.row_end])
         self.n = shard.n_local
         self.row_ptr = shard.local_row_ptr
         self.col_idx = shard.local_col_idx
-        self.values = np.ascontiguousarray(np.asarray(A.values)[e0:e1], dtype=np.float64)
+        self.values = np.ascontiguousarray(np.asarray(values)[e0:e1], dtype=np.float64)
 
 
 class ShardedEngine(DeviceEngine):
-    def __init__(self, op, partition, cfg, comm=None, device=None):
+    """decomposition: "subdomain" (CSR: rows renumbered subdomain-major, whole
+    t-subdomains per rank, dist.subdomain_order; needs t % G == 0) or "rows"
+    (balanced contiguous row ranges); stencil operators always shard by layers."""
+
+    def __init__(self, op, partition, cfg, comm=None, device=None, decomposition="subdomain", overlap=True):
         if cfg.preconditioner is not None:
             raise ValueError("the sharded engine runs unpreconditioned")
         if cfg.method not in ("sre-cg2", "sre-cg") or cfg.switch_tol is not None:
             raise ValueError("the sharded engine runs SRE-CG2 / SRE-CG without the flexible switch")
         comm = comm if comm is not None else Comm()
         self.stencil = isinstance(op, StencilOperator)
+        self.order = None  # new row i = global row order[i] (CSR subdomain decomposition)
+        self.overlap = overlap  # run interior rows while the halo is exchanged
         if self.stencil:
             shard = RowShard(op.shape, comm.rank, comm.world)
             local_op = op
@@ -63,8 +70,17 @@ class ShardedEngine(DeviceEngine):
             host = op.host if isinstance(op, CsrOperator) else op
             if not all(hasattr(host, a) for a in ("n", "row_ptr", "col_idx", "values")):
                 raise TypeError("the sharded engine needs a StencilOperator or a CSR matrix")
-            shard = CsrShard(host.row_ptr, host.col_idx, comm.rank, comm.world).plan(comm)
-            local_op = CsrOperator(_LocalCsr(host, shard), device)
+            rp, ci, vals = host.row_ptr, host.col_idx, host.values
+            bounds = None
+            plan = (subdomain_order(partition.owner(), partition.t, comm.world, rp, ci)
+                    if decomposition == "subdomain" else None)
+            if plan is not None:
+                self.order, bounds = plan
+                rp, ci, vals = permute_csr(rp, ci, vals, self.order)
+                partition = Partition.from_owner(np.asarray(partition.owner())[self.order], partition.t)
+            shard = CsrShard(rp, ci, comm.rank, comm.world, bounds=bounds).plan(comm)
+            local_op = CsrOperator(_LocalCsr(rp, vals, shard), device)
+        self.decomposition = "layers" if self.stencil else ("subdomain" if self.order is not None else "rows")
         super().__init__(local_op, partition, cfg, device=device)
         self.comm = comm
         self.shard = shard
@@ -74,12 +90,29 @@ class ShardedEngine(DeviceEngine):
         self.n = self.shard.n_local  # every row-local kernel works on the local rows
         self.cache_aq = "auto"  # the lean scheme when the cached one does not fit the local HBM
         if self.stencil:
-            desc = _lib.EkcgStencil()
-            ctypes.memmove(ctypes.byref(desc), ctypes.byref(op._desc), ctypes.sizeof(desc))
-            desc.row_begin, desc.row_end = self.shard.row_begin, self.shard.row_end
-            self._desc = desc
+            self._desc = self._desc_rows(op, self.shard.row_begin, self.shard.row_end)
+            interior, boundary = self.shard.row_ranges()
+            self._desc_int = None if interior is None else self._desc_rows(op, *interior)
+            self._desc_bnd = [self._desc_rows(op, a, b) for a, b in boundary]
         else:
             self.send_idx = {q: torch.from_numpy(v).to(self.device) for q, v in shard.send.items()}
+        self._order_t = None if self.order is None else torch.from_numpy(self.order)
+
+    @staticmethod
+    def _desc_rows(op, r0, r1):
+        desc = _lib.EkcgStencil()
+        ctypes.memmove(ctypes.byref(desc), ctypes.byref(op._desc), ctypes.sizeof(desc))
+        desc.row_begin, desc.row_end = r0, r1
+        return desc
+
+    def _global_to_local(self, v):
+        """This rank's rows of a global vector (numpy or torch), in the engine's row order."""
+        v = torch.as_tensor(v, dtype=torch.float64)
+        if v.numel() != self.n_global:
+            return v
+        if self._order_t is not None:
+            v = v[self._order_t.to(v.device)]
+        return v[self.shard.row_begin:self.shard.row_end]
 
     # ------------------------------------------------------------ pointers
     def _lptr(self, ext, ld):
@@ -92,10 +125,37 @@ class ShardedEngine(DeviceEngine):
 
     def _exchange(self, ext, ld):
         """Fill the halo rows of an extended block from the peers that own them."""
+        self.comm.wait(self._exchange_start(ext, ld))
+
+    def _exchange_start(self, ext, ld):
         if self.stencil:
-            self.comm.halo_exchange(ext, ld, self.shard)
+            return self.comm.halo_exchange_start(ext, ld, self.shard)
+        return self.comm.csr_exchange_start(ext, ld, self.shard, self.send_idx)
+
+    def _exchange_apply(self, ext, col, ldx, y_loc, ldy, m, live):
+        """Y_local = A X for columns [col, col + m) of the extended block `ext`:
+        start the halo exchange, run the interior rows (no halo reads) while it is
+        in flight, then wait and run the boundary rows.  The sends read the local
+        rows and the receives write only the halo, so the interior product and the
+        exchange touch disjoint data; the result equals one whole-shard product
+        bit for bit (every row is computed by the same kernel arithmetic)."""
+        works = self._exchange_start(ext, ldx)
+        interior, boundary = self.shard.row_ranges()
+        if not self.overlap or interior is None or works is None:
+            self.comm.wait(works)
+            self._apply_ext(ext, col, ldx, y_loc, ldy, m, live)
+            return
+        self._apply_rows(ext, col, ldx, y_loc, ldy, m, live, interior, self._desc_int if self.stencil else None)
+        self.comm.wait(works)
+        for j, rng in enumerate(boundary):
+            self._apply_rows(ext, col, ldx, y_loc, ldy, m, live, rng, self._desc_bnd[j] if self.stencil else None)
+
+    def _apply_rows(self, ext, col, ldx, y_loc, ldy, m, live, rng, desc):
+        if self.stencil:
+            _lib.call("ekcg_spmm_stencil", ctypes.byref(desc), self._gptr_ext(ext, ldx) + F64 * col, ldx,
+                      y_loc - F64 * self.shard.row_begin * ldy, ldy, m, live, self.stream)
         else:
-            self.comm.csr_exchange(ext, ld, self.shard, self.send_idx)
+            self.op.apply_rows(rng[0], rng[1], ext.data_ptr() + F64 * col, ldx, y_loc, ldy, m, live, self.stream)
 
     def _apply_ext(self, ext, col, ldx, y_loc, ldy, m, live):
         """Y_local = A X for columns [col, col + m) of the extended block `ext`
@@ -157,16 +217,10 @@ class ShardedEngine(DeviceEngine):
     # --------------------------------------------------------- residuals
     def _begin(self, b, x0):
         dev, st, sh = self.device, self.stream, self.shard
-        b = torch.as_tensor(b, dtype=torch.float64)
-        if b.numel() == self.n_global:
-            b = b[sh.row_begin:sh.row_end]
-        self.b = b.to(dev).contiguous()
+        self.b = self._global_to_local(b).to(dev).contiguous()
         self.x = torch.zeros(sh.ext_rows, dtype=torch.float64, device=dev)
         if x0 is not None:
-            x0 = torch.as_tensor(x0, dtype=torch.float64)
-            if x0.numel() == self.n_global:
-                x0 = x0[sh.row_begin:sh.row_end]
-            self.x[sh.lo:sh.lo + sh.n_local].copy_(x0.to(dev))
+            self.x[sh.lo:sh.lo + sh.n_local].copy_(self._global_to_local(x0).to(dev))
         self.r = torch.empty(self.n, dtype=torch.float64, device=dev)
         self._residual_sq(self.x, self.rho2, None, store_r=True)
         _lib.call("ekcg_start", self.ctrl.data_ptr(), self.rho2.data_ptr(), self.tol, self.history.data_ptr(), st)
@@ -174,8 +228,7 @@ class ShardedEngine(DeviceEngine):
     def _residual_sq(self, x, out, live, store_r=False):
         """out = |b - A x|^2 over all ranks (x extended with halos)."""
         st = self.stream
-        self._exchange(x, 1)
-        self._apply_ext(x, 0, 1, self.tmpv.data_ptr(), 1, 1, live)
+        self._exchange_apply(x, 0, 1, self.tmpv.data_ptr(), 1, 1, live)
         dst = self.r if store_r else self.tmpv
         _lib.call("ekcg_sub", self.b.data_ptr(), self.tmpv.data_ptr(), dst.data_ptr(), self.n, live, st)
         _lib.call("ekcg_sumsq", dst.data_ptr(), self.n, self.vpart.data_ptr(), live, st)
@@ -188,7 +241,7 @@ class ShardedEngine(DeviceEngine):
         rel = None
         if x_star is not None:
             sh = self.shard
-            xs = torch.as_tensor(x_star, dtype=torch.float64)[sh.row_begin:sh.row_end].to(self.device)
+            xs = self._global_to_local(x_star).to(self.device)
             xl = self.x[sh.lo:sh.lo + sh.n_local]
             sums = torch.stack([torch.sum((xl - xs) ** 2), torch.sum(xs ** 2)])
             self.comm.allreduce_(sums)
@@ -198,6 +251,10 @@ class ShardedEngine(DeviceEngine):
     def _output_x(self, numpy_io):
         sh = self.shard
         full = self.comm.gather_rows(self.x[sh.lo:sh.lo + sh.n_local].contiguous(), sh)
+        if self._order_t is not None:  # back to the caller's row numbering
+            out = torch.empty_like(full)
+            out[self._order_t.to(full.device)] = full
+            full = out
         return full.cpu().numpy() if numpy_io else full
 
     def _state(self, k, rho, tol1, numpy_io):
@@ -230,8 +287,7 @@ class ShardedEngine(DeviceEngine):
         if d > 0:
             C = self._ensure("C", d * m * m)
             for _ in range(2):  # C = Q^T (A W), A symmetric (engine._enqueue_iteration_lean)
-                self._exchange(self.WA, m)
-                self._apply_ext(self.WA, 0, m, lWC, m, m, live)
+                self._exchange_apply(self.WA, 0, m, lWC, m, m, live)
                 self._gram(q_addr(0), m, d, m, lWC, m, m, C.data_ptr(), tag="hist_gram")
                 self.comm.allreduce_(C[: d * m * m])
                 self._update(q_addr(0), m, d, m, C.data_ptr(), lWA, m, lWA, m, m, 1.0, -1.0, tag="hist_update")
@@ -239,16 +295,14 @@ class ShardedEngine(DeviceEngine):
         self.comm.allreduce_(self.Graw[: m * m])
         _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
         self._tri_apply(WA_arr, m, self.S0.data_ptr(), lWC, m, m)  # W0 -> WC
-        self._exchange(self.WC, m)
-        self._apply_ext(self.WC, 0, m, lWA, m, m, live)  # A W0 -> WA (free)
+        self._exchange_apply(self.WC, 0, m, lWA, m, m, live)  # A W0 -> WA (free)
         self._gram(WC_arr, m, 1, m, lWA, m, m, self.G.data_ptr(), tag="gram_aw")
         self.comm.allreduce_(self.G[: m * m])
         _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
         self._tri_apply(WC_arr, m, self.S.data_ptr(), lq(blk), m, m)
         self._gram(NEW_arr, m, 1, m, self.r.data_ptr(), 1, 1, self.alpha.data_ptr(), tag="gram_vec")
         self.comm.allreduce_(self.alpha[:m])
-        self._exchange(blk.q, m)
-        self._apply_ext(blk.q, 0, m, lWA, m, m, live)  # A W_k -> WA: the next candidate
+        self._exchange_apply(blk.q, 0, m, lWA, m, m, live)  # A W_k -> WA: the next candidate
         _lib.call("ekcg_xr_update", lq(blk), m, lWA, m, self.alpha.data_ptr(), m, self._lptr(self.x, 1),
                   self.r.data_ptr(), n, self.vpart.data_ptr(), live, st)
         _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
@@ -316,17 +370,17 @@ class ShardedEngine(DeviceEngine):
         self.comm.allreduce_(self.Graw[: m * m])
         _lib.call("ekcg_prechol", self.Graw.data_ptr(), m, self.S0.data_ptr(), live, k, 1e-14, st)
         self._tri_apply(WA_arr, m, self.S0.data_ptr(), lWB, m, m)
-        self._exchange(self.WB, m)
         fused = m in (8, 16, 32, 64)
         # same kernel choice as DeviceEngine: the fused stencil kernels only for
         # m <= 16, the plane-marching stencil + DMMA kernels above (CSR: unfused)
         fused_st = fused and m <= 16 and self.stencil
         part = self._ensure("part", max(self.fused_part, 1)) if fused else None
         if fused_st:
+            self._exchange(self.WB, m)
             _lib.call("ekcg_stencil_cholinv", ctypes.byref(self._desc), self._gptr_ext(self.WB, m), m, m,
                       part.data_ptr(), self.counter.data_ptr(), self.G.data_ptr(), live, k, 1e-14, 0, st)
         else:
-            self._apply_ext(self.WB, 0, m, self.WC.data_ptr(), m, m, live)
+            self._exchange_apply(self.WB, 0, m, self.WC.data_ptr(), m, m, live)
             self._gram(WB_arr, m, 1, m, self.WC.data_ptr(), m, m, self.G.data_ptr(), tag="gram_aw")
         self.comm.allreduce_(self.G[: m * m])
         _lib.call("ekcg_cholinv", self.G.data_ptr(), m, self.S.data_ptr(), live, k, 1e-14, st)
@@ -339,14 +393,14 @@ class ShardedEngine(DeviceEngine):
         self.comm.allreduce_(self.alpha[:m])
 
         # ---- AW_k = A W_k and the iterate update ----
-        self._exchange(blk.q, m)
         if fused_st:
+            self._exchange(blk.q, m)
             _lib.call("ekcg_stencil_xr", ctypes.byref(self._desc), self._gptr_ext(blk.q, m), m,
                       self._gptr_loc(blk.aq, m), m, m, self.alpha.data_ptr(), self._gptr_ext(self.x, 1),
                       self._gptr_loc(self.r, 1), part.data_ptr(), self.counter.data_ptr(), live, k, self.kmax,
                       self.stag_window, self.history.data_ptr(), 0, self.rho2.data_ptr(), st)
         else:
-            self._apply_ext(blk.q, 0, m, blk.aq.data_ptr(), m, m, live)
+            self._exchange_apply(blk.q, 0, m, blk.aq.data_ptr(), m, m, live)
             _lib.call("ekcg_xr_update", lq(blk), m, blk.aq.data_ptr(), m, self.alpha.data_ptr(), m,
                       self._lptr(self.x, 1), self.r.data_ptr(), n, self.vpart.data_ptr(), live, st)
             _lib.call("ekcg_reduce", self.vpart.data_ptr(), self.vchunks, 1, self.rho2.data_ptr(), live, st)
@@ -364,5 +418,4 @@ class ShardedEngine(DeviceEngine):
 
     def _chain_sharded(self, m, t, live):
         for i in range(1, self.s):
-            self._exchange(self.WA, m)
-            self._apply_ext(self.WA, (i - 1) * t, m, self._lptr(self.WA, m) + F64 * i * t, m, t, live)
+            self._exchange_apply(self.WA, (i - 1) * t, m, self._lptr(self.WA, m) + F64 * i * t, m, t, live)

@@ -16,8 +16,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import ekcg_oracle as orc
-from paper_2305_19013_b200.dist import Comm, CsrShard, RowShard, row_bounds
-from paper_2305_19013_b200.problems import diffusion_csr
+from paper_2305_19013_b200.dist import Comm, CsrShard, RowShard, permute_csr, row_bounds, subdomain_order
+from paper_2305_19013_b200.problems import box_owner, diffusion_csr
 
 
 def _free_port():
@@ -127,14 +127,26 @@ def _csr_worker(rank, world, port, kind, m, q):
     try:
         comm = Comm()
         rng = np.random.default_rng(11)
-        if kind == "grid":
-            A = diffusion_csr((5, 4, 6), np.exp(rng.uniform(-2, 2, 120)))
+        bounds = None
+        if kind in ("grid", "subdomain"):
+            A = diffusion_csr((8, 4, 6), np.exp(rng.uniform(-2, 2, 192)))
             rp, ci, vals = A.row_ptr, A.col_idx, A.values
         else:
             rp, ci, vals = _random_spd_csr(90, rng)
         n = len(rp) - 1
         X = rng.standard_normal((n, m))
-        sh = CsrShard(rp, ci, rank, world).plan(comm)
+        if kind == "subdomain":  # 4 x 2 x 2 boxes, whole subdomains per rank, interior rows first
+            owner = box_owner((8, 4, 6), (4, 2, 2))
+            order, bounds = subdomain_order(owner, 16, world, rp, ci)
+            rp0, ci0, vals0 = rp, ci, vals
+            rp, ci, vals = permute_csr(rp, ci, vals, order)
+            # P A P^T keeps every row's products: the permuted product is the original's rows, bitwise
+            assert np.array_equal(orc.csr_spmm(rp, ci, vals, X[order]), orc.csr_spmm(rp0, ci0, vals0, X)[order])
+            X = X[order]
+            per = 16 // world
+            sub = owner[order]
+            assert all(set(sub[bounds[p]:bounds[p + 1]] // per) == {p} for p in range(world))
+        sh = CsrShard(rp, ci, rank, world, bounds=bounds).plan(comm)
         ext = torch.zeros(sh.ext_rows * m, dtype=torch.float64)
         ext.view(sh.ext_rows, m)[sh.lo:sh.lo + sh.n_local] = torch.from_numpy(X[sh.row_begin:sh.row_end])
         comm.csr_exchange(ext, m, sh, {q_: torch.from_numpy(v) for q_, v in sh.send.items()})
@@ -146,6 +158,17 @@ def _csr_worker(rank, world, port, kind, m, q):
         Y_loc = np.add.reduceat(vals[e0:e1][:, None] * E[lci], sh.local_row_ptr[:-1], axis=0)  # linalg.py:150
         Y_ref = orc.csr_spmm(rp, ci, vals, X)[sh.row_begin:sh.row_end]
         prod_ok = np.array_equal(Y_loc.view(np.int64), Y_ref.view(np.int64))  # same association: bitwise
+        # interior rows reference no halo row (they run while the exchange is in flight)
+        interior, boundary = sh.row_ranges()
+        if interior is not None:
+            a, b = interior
+            seg = lci[sh.local_row_ptr[a]:sh.local_row_ptr[b]]
+            prod_ok &= bool(np.all((seg >= sh.lo) & (seg < sh.lo + sh.n_local)))
+            covered = sorted([interior] + boundary)
+            prod_ok &= covered[0][0] == 0 and covered[-1][1] == sh.n_local and all(
+                x[1] == y[0] for x, y in zip(covered, covered[1:]))
+            if kind == "subdomain":
+                prod_ok &= a == 0 and b > 0  # interior-first numbering
         full = comm.gather_rows(torch.from_numpy(X[sh.row_begin:sh.row_end, 0].copy()), sh)
         gather_ok = np.array_equal(full.numpy(), X[:, 0])
         q.put((rank, bool(halo_ok), bool(prod_ok), bool(gather_ok)))
@@ -153,7 +176,8 @@ def _csr_worker(rank, world, port, kind, m, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,kind", [(2, "grid"), (3, "grid"), (2, "random"), (3, "random")])
+@pytest.mark.parametrize("world,kind", [(2, "grid"), (3, "grid"), (2, "random"), (3, "random"),
+                                        (2, "subdomain"), (4, "subdomain")])
 def test_csr_sharded_dataflow_gloo(world, kind):
     """CSR row shards: the halo plan (requests exchanged once), the per-product exchange
     and a local product on [lo halo | local | hi halo] that equals the global rows bitwise."""
@@ -179,3 +203,22 @@ def test_csr_shard_single_rank_and_bounds():
     assert list(b) == [0, 4, 7, 10]
     with pytest.raises(ValueError):
         row_bounds(2, 3)
+
+
+def test_stencil_row_ranges_cover_the_slab():
+    for world in (1, 2, 4):
+        for r in range(world):
+            sh = RowShard((6, 5, 16), r, world)
+            interior, boundary = sh.row_ranges()
+            rngs = sorted(([interior] if interior else []) + boundary)
+            assert rngs[0][0] == sh.row_begin and rngs[-1][1] == sh.row_end
+            assert all(x[1] == y[0] for x, y in zip(rngs, rngs[1:]))
+            if interior:  # the interior's stencil neighbours stay inside the slab
+                assert interior[0] - sh.plane >= sh.row_begin or not sh.has_lo
+                assert interior[1] + sh.plane <= sh.row_end or not sh.has_hi
+
+
+def test_subdomain_order_needs_divisible_t():
+    assert subdomain_order(np.zeros(10, dtype=np.int64), 3, 2) is None
+    order, bounds = subdomain_order(np.repeat(np.arange(4), 5)[::-1].copy(), 4, 2)
+    assert list(bounds) == [0, 10, 10 + 10] and sorted(order) == list(range(20))
