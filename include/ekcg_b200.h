@@ -11,6 +11,12 @@
  * reads 0 the kernel returns immediately; the solver's finalize kernel clears
  * it so iterations enqueued ahead of the host's status poll retire empty.
  *
+ * The library is stateless: it holds no tunable or per-solve state.  Which
+ * kernel a call launches, its grid and its split-K chunk count are functions
+ * of the call's arguments (sizes, strides, pointer alignment) and of the
+ * device it runs on; per-device launch set-up (shared-memory limits,
+ * occupancy) is cached per device ordinal.  Calls are re-entrant per stream.
+ *
  * The reference (`ekcg`, pure Python) has no FFI; each entry replaces the
  * numpy/scipy call cited beside it (paths relative to pkg/src/ekcg/).  The
  * Python driver binds these with ctypes (paper_2305_19013_b200/_lib.py);
@@ -80,10 +86,25 @@ int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const double* va
                   const double* X, int ldx, double* Y, int ldy, long long n, int m,
                   const int* live, void* stream);
 
+/* ekcg_spmm_csr with an explicit kernel form, for cross-checks of the forms
+ * against each other (all are bit-identical): 0 = automatic (ekcg_spmm_csr),
+ * 1 = software-pipelined (256-bit gathers when 32-B aligned), 2 = pipelined
+ * with 128-bit accesses, 3 = 4 columns per thread, 4 = 2 columns per thread,
+ * 5 = one thread per (row, column).  -1 when the form does not apply. */
+int ekcg_spmm_csr_kernel(int form, const long long* row_ptr, const int* col_idx, const double* values,
+                         const double* X, int ldx, double* Y, int ldy, long long n, int m,
+                         const int* live, void* stream);
+
 /* Y = A X for the grid stencil operator; bit-exact with ekcg_spmm_csr on the
  * CSR that generators.py:25-60 assembles for the same kappa. */
 int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
                       int m, const int* live, void* stream);
+
+/* ekcg_spmm_stencil with an explicit kernel form: 0 = automatic, 1 = the TMA
+ * plane march at any size (-1 when it does not apply: m % 4, alignment, or a
+ * row range that is not whole planes), 2 = the row-parallel kernel. */
+int ekcg_spmm_stencil_kernel(int form, const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
+                             int m, const int* live, void* stream);
 
 /* ---- tall-skinny block products (aortho.py:92-94,105,108; solvers.py:394-396) */
 
@@ -224,11 +245,6 @@ int ekcg_finish(void* ctrl, const double* rho2, int k, int kmax, int stagnation_
 
 /* checks[slot] = sqrt(*rho2) when the solve is live (true residual log, solvers.py:401-402). */
 int ekcg_store_norm(const double* rho2, double* checks, int slot, const int* live, void* stream);
-
-/* Performance knobs (results are unchanged up to summation order):
- * key 1 = m=16 Gram variant (-1 auto, 0..6), key 2 = target CTA count of the Gram grid (0 auto).
- * Call before a solve; ekcg_gram_chunks reflects the setting. */
-int ekcg_tune(int key, long long value);
 
 /* Kernel launches issued through this library since load. */
 unsigned long long ekcg_launch_count(void);

@@ -23,6 +23,10 @@ SIGNATURES = {
     "ekcg_spmm_csr": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int, c_longlong,
                               c_int, c_void_p, c_void_p]),
     "ekcg_spmm_stencil": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p]),
+    "ekcg_spmm_csr_kernel": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int,
+                                     c_longlong, c_int, c_void_p, c_void_p]),
+    "ekcg_spmm_stencil_kernel": (c_int, [c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p,
+                                         c_void_p]),
     "ekcg_gram_chunks": (c_int, [c_longlong, c_int, c_int, c_int]),
     "ekcg_gram": (c_int, [c_void_p, c_int, c_int, c_int, c_void_p, c_int, c_int, c_longlong, c_void_p,
                           c_void_p, c_void_p]),
@@ -48,7 +52,6 @@ SIGNATURES = {
     "ekcg_finish": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_void_p, c_void_p]),
     "ekcg_store_norm": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p]),
     "ekcg_launch_count": (c_uint64, []),
-    "ekcg_tune": (c_int, [c_int, c_longlong]),
     "ekcg_fused_partials": (c_int, [c_longlong, c_int]),
     "ekcg_update_prechol": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int,
                                     c_longlong, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_double, c_void_p]),

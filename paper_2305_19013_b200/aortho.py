@@ -14,7 +14,7 @@ import torch
 
 from . import _lib
 from .device import as_device, current_stream_ptr
-from .linalg import Breakdown, _ptr_table, cholesky_small, gram, spmm, trsm_right_inv
+from .linalg import Breakdown, _aligned, _ptr_table, cholesky_small, gram, spmm, trsm_right_inv
 
 __all__ = ["a_orthogonalize_against", "a_cholqr", "pre_cholqr"]
 
@@ -29,7 +29,7 @@ def _sub_product(W, Q, C):
     k = Q.shape[1]
     out = torch.empty_like(W)
     if n:
-        Qc = Q.contiguous()
+        Qc = _aligned(Q.contiguous())
         tab = _ptr_table(Qc)
         _lib.call("ekcg_block_update", tab.data_ptr(), k, 1, k, C.contiguous().data_ptr(), W.data_ptr(), m,
                   out.data_ptr(), m, m, 1.0, -1.0, n, None, current_stream_ptr(W.device))

@@ -33,9 +33,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
             return;                             \
     } while (0)
 
-extern int g_pdl;  // 0: plain launches, 1: PDL attribute (ekcg_tune key 14)
-
-// <<<>>> replacement that adds the PDL launch attribute when enabled.
+// <<<>>> replacement that adds the programmatic-dependent-launch attribute
+// (back-to-back launch floor 5.2 -> 3.2 us on B200).
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                                    Args... args) {
@@ -46,13 +45,67 @@ static inline cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 blo
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = g_pdl ? 1 : 0;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
 
 static inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---------------------------------------------------------------------------
+// Per-device launch set-up.  The library holds no tunable state: every kernel
+// choice and split count is a function of the call's arguments and of the
+// device it runs on.  What is cached is per device ordinal -- the SM count
+// and, per kernel instance, the raised dynamic shared-memory limit and its
+// occupancy -- so a process driving several GPUs sets each one up.
+// ---------------------------------------------------------------------------
+constexpr int kEkcgMaxDevices = 64;
+
+static inline int ekcg_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kEkcgMaxDevices) {
+        cudaGetLastError();
+        d = 0;
+    }
+    return d;
+}
+
+static inline int device_sms() {
+    static int sms[kEkcgMaxDevices];
+    const int d = ekcg_device();
+    if (sms[d] == 0) {
+        int v = 148;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v < 1) {
+            cudaGetLastError();
+            v = 148;
+        }
+        sms[d] = v;
+    }
+    return sms[d];
+}
+
+// Resident CTAs per SM of `fn` at (threads, smem) on the current device, after
+// raising its dynamic shared-memory limit there; 0 when it cannot launch.
+// `cache` is a per-kernel-instance array of kEkcgMaxDevices ints (static at the call site).
+template <typename F>
+static inline int kernel_occupancy(F fn, int threads, size_t smem, int* cache) {
+    const int d = ekcg_device();
+    if (cache[d] == 0) {
+        int occ = 0;
+        if (smem > 48 * 1024 &&
+            cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+                cudaSuccess) {
+            cudaGetLastError();
+        } else if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, threads, smem) !=
+                   cudaSuccess) {
+            cudaGetLastError();
+            occ = 0;
+        }
+        cache[d] = occ + 1;  // 1 = set up, cannot launch
+    }
+    return cache[d] - 1;
+}
 
 static inline int launch_status() {
     cudaError_t e = cudaGetLastError();

@@ -27,41 +27,20 @@ long long rows_per_chunk(long long n, int chunks) {
     return ((r + 15) / 16) * 16;
 }
 
-// Tuning knobs (ekcg_tune): m = 16 Gram variant and target CTA count.
-int g_gram16_variant = -1;   // -1: automatic by d (measured on B200, tools/tune_gram.py)
-long long g_gram_target = 0;  // 0: automatic
 }  // namespace
 int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
                        int chunks, long long rows_chunk, double* partials, const int* live, cudaStream_t st);
-extern int g_gram_stream;
-extern int g_gram16_d1;
+int gram16_stream_slots(int d);
 int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
                          double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                          cudaStream_t st);
-extern int g_update_stream;
-extern int g_wide_stream;
-extern int g_csr_vec;
-extern int g_csr_w256;
-extern int g_wide_upd_variant;
 int gram_wide_slots(int gb);
 int launch_gram_wide(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
                      int chunks, long long rows_chunk, int gb, double* partials, const int* live, cudaStream_t st);
 int launch_update_wide_any(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
                            double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                            cudaStream_t st);
-extern int g_march_fused;
-extern int g_fused_variant;
-
-int g_stencil_march = 1;      // plane-marching stencil kernel on/off (sparse.cu)
-int g_march_variant = 0;      // plane-marching tile/stage variant (stencil_march.cu)
-long long g_march_min_work = 1LL << 21;
-int g_pdl = 1;  // programmatic dependent launch on (ekcg_tune key 14)
-int g_vec256 = 1;  // ekcg_tune key 24: 256-bit row loads in the x/r update and X^T y when 32-B aligned
-int g_tri_skip = 1;  // ekcg_tune key 18: ekcg_tri_apply skips the zero blocks of S (m = 64)
-int g_upd_il = 0;             // interleaved k-pair loads in the DMMA update (A/B knob)
-int g_frag_il = -1;           // interleaved 16-B fragment loads in the DMMA Gram: -1 auto, 0 off, 1 on
 namespace {
-constexpr int kGram16GB[] = {4, 2, 2, 4, 4, 4, 1};
 
 // Blocks per CTA that share one pass over Y (see gram_dmma_kernel).
 int gram_blocks_per_cta(int d, int m1, int m2) {
@@ -69,7 +48,7 @@ int gram_blocks_per_cta(int d, int m1, int m2) {
     int gb = 1;
     switch (m1) {
         case 8: gb = 8; break;
-        case 16: gb = g_gram16_variant >= 0 ? kGram16GB[g_gram16_variant] : 4; break;
+        case 16: gb = 4; break;
         case 32: gb = 2; break;
         default: gb = 1;
     }
@@ -225,7 +204,7 @@ GramFn select_gram(int d, int m1, int m2, int& gb) {
     gb = gram_blocks_per_cta(d, m1, m2);
     // interleaved loads: faster for m = 32 and for m = 16 with short histories,
     // slower for m = 16 with d >= 48 and for m = 64 (tools/kernel_times.py)
-    const bool il = g_frag_il >= 0 ? g_frag_il == 1 : (m1 == 32 || (m1 == 16 && d < 48));
+    const bool il = m1 == 32 || (m1 == 16 && d < 48);
     if (m1 != m2) return nullptr;
     switch (m1) {
         case 8:
@@ -233,16 +212,12 @@ GramFn select_gram(int d, int m1, int m2, int& gb) {
             if (gb == 4) return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 4, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 4, false>;
             if (gb == 2) return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 2, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 2, false>;
             return il ? (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 1, true> : (GramFn)gram_dmma_kernel<8, 1, 1, 4, 4, 1, false>;
-        case 16: {
-            const int v = g_gram16_variant >= 0 ? g_gram16_variant : (d >= 48 ? 0 : 3);
+        case 16:
+            // 4 blocks per CTA: 2 k-step lanes for long histories (d >= 48), 1 below (tools/tune_gram.py)
             if (gb == 1) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 1, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 1, false>;
-            if ((v == 1 || g_gram16_variant < 0) && gb == 2) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 2, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 2, false>;
-            if (gb == 2) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 2, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 2, false>;
-            if (v == 3 && gb == 4) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 1, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 1, 4, false>;
-            if (v == 5 && gb == 4) return il ? (GramFn)gram_dmma_kernel<16, 2, 1, 2, 4, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 1, 2, 4, 4, false>;
-            if (v == 4 && gb == 4) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 4, false>;
+            if (gb == 2) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 2, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 4, 2, false>;
+            if (d < 48) return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 1, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 1, 4, false>;
             return il ? (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 4, true> : (GramFn)gram_dmma_kernel<16, 2, 2, 4, 2, 4, false>;
-        }
         case 32:
             if (gb == 2) return il ? (GramFn)gram_dmma_kernel<32, 4, 2, 2, 2, 2, true> : (GramFn)gram_dmma_kernel<32, 4, 2, 2, 2, 2, false>;
             return il ? (GramFn)gram_dmma_kernel<32, 4, 2, 2, 4, 1, true> : (GramFn)gram_dmma_kernel<32, 4, 2, 2, 4, 1, false>;
@@ -256,36 +231,35 @@ GramFn select_gram(int d, int m1, int m2, int& gb) {
 // Resident CTAs per SM of a Gram kernel (queried once per variant; 4 when no
 // device is present, e.g. host-only queries).
 int gram_occupancy(GramFn fn) {
-    static GramFn keys[64];
-    static int vals[64];
+    constexpr int kMax = 64;
+    static GramFn keys[kMax];
+    static int vals[kMax][kEkcgMaxDevices];
     static int used = 0;
     if (fn == nullptr) return 4;
+    int slot = -1;
     for (int i = 0; i < used; ++i)
-        if (keys[i] == fn) return vals[i];
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, (const void*)fn, kGramThreads, 0) != cudaSuccess ||
-        occ < 1) {
-        cudaGetLastError();
-        return 4;
+        if (keys[i] == fn) slot = i;
+    if (slot < 0) {
+        if (used == kMax) return 4;
+        slot = used;
+        keys[used++] = fn;
     }
-    if (used < 64) {
-        keys[used] = fn;
-        vals[used++] = occ;
-    }
-    return occ;
+    const int occ = kernel_occupancy(fn, kGramThreads, 0, vals[slot]);
+    return occ < 1 ? 4 : occ;
 }
 
 int gram_chunks(long long n, int d, int m1, int m2) {
     int gb;
     GramFn fn = select_gram(d, m1, m2, gb);
     const long long groups = (d + gb - 1) / gb;
-    const bool wide = m1 == 32 && m2 == 32 && g_wide_stream && g_gram_target <= 0;
-    if ((m1 == 16 && m2 == 16 && g_gram_stream && g_gram_target <= 0) || wide) {
+    const bool wide = m1 == 32 && m2 == 32;
+    if ((m1 == 16 && m2 == 16) || wide) {
         // streamed Gram: resident CTAs with long row ranges.  Pick the chunk
         // count whose CTA total fills its last wave best (equal work per CTA),
         // preferring fewer chunks; at least 1024 rows per chunk.
-        const bool d1 = !wide && d == 1 && g_gram16_d1;  // GB = 1 stream kernel: 3 CTAs per SM
-        const long long slots = wide ? gram_wide_slots(gb) : d1 ? 3 * 148 : (g_gram_stream >= 9 ? 2 * 148 : 148);
+        const bool d1 = !wide && d == 1;  // GB = 1 stream kernel
+        long long slots = wide ? gram_wide_slots(gb) : gram16_stream_slots(d);  // co-resident CTAs of that kernel
+        if (slots < 1) slots = device_sms();
         long long pmax = (n + (d1 ? 511 : 1023)) / (d1 ? 512 : 1024);
         const long long cap = (4 * slots + groups - 1) / groups;
         if (pmax > cap) pmax = cap;
@@ -302,11 +276,8 @@ int gram_chunks(long long n, int d, int m1, int m2) {
         }
         return (int)best;
     }
-    long long target = g_gram_target;
-    if (target <= 0) {
-        const long long waves = (m1 == 16 && m2 == 16 && d >= 48) ? 2 : 1;
-        target = 148LL * gram_occupancy(fn) * waves;
-    }
+    const long long waves = (m1 == 16 && m2 == 16 && d >= 48) ? 2 : 1;
+    const long long target = (long long)device_sms() * gram_occupancy(fn) * waves;
     long long p = target / groups;  // floor: whole waves, no straggler CTAs
     long long max_p = (n + 255) / 256;
     if (p > max_p) p = max_p;
@@ -650,6 +621,8 @@ __global__ void update_generic_kernel(const double* const* __restrict__ Qs, int 
 // ---------------------------------------------------------------------------
 // vector kernels with deterministic block partial sums
 // ---------------------------------------------------------------------------
+// A fixed cap (not the device's SM count): the chunk count sets the summation order, so norms are
+// bit-identical on every B200 regardless of its SM count.
 int vec_chunks(long long n) {
     long long p = (n + kVecThreads - 1) / kVecThreads;
     if (p > 148LL * 8) p = 148LL * 8;
@@ -887,86 +860,6 @@ __global__ void sub_kernel(const double* __restrict__ a, const double* __restric
 // ---------------------------------------------------------------------------
 // C ABI
 // ---------------------------------------------------------------------------
-extern "C" int ekcg_tune(int key, long long value) {
-    if (key == 1 && value >= -1 && value < (long long)(sizeof(kGram16GB) / sizeof(int))) {
-        g_gram16_variant = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 2 && value >= 0) {
-        g_gram_target = value;
-        return EKCG_OK;
-    }
-    if (key == 3 && value >= 0 && value <= 1) {
-        g_stencil_march = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 18 && value >= 0 && value <= 1) {
-        g_tri_skip = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 17 && value >= 0 && value <= 3) {
-        g_csr_vec = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 24 && (value == 0 || value == 1)) {
-        g_vec256 = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 22 && (value == 0 || value == 1)) {
-        g_csr_w256 = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 21 && value >= 0 && value <= 4) {
-        g_gram16_d1 = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 16 && value >= 0 && value <= 2) {
-        g_wide_upd_variant = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 15 && value >= 0 && value <= 1) {
-        g_wide_stream = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 14 && value >= 0 && value <= 1) {
-        g_pdl = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 13 && value >= 0 && value <= 6) {
-        g_fused_variant = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 12 && value >= 0) {
-        g_march_min_work = value;
-        return EKCG_OK;
-    }
-    if (key == 9 && value >= 0 && value <= 1) {
-        g_march_fused = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 8 && value >= 0 && value <= 7) {
-        g_update_stream = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 7 && value >= 0 && value <= 10) {
-        g_gram_stream = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 6 && value >= 0 && value <= 1) {
-        g_upd_il = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 5 && value >= -1 && value <= 1) {
-        g_frag_il = (int)value;
-        return EKCG_OK;
-    }
-    if (key == 4 && value >= 0 && value <= 6) {
-        g_march_variant = (int)value;
-        return EKCG_OK;
-    }
-    return EKCG_EINVAL;
-}
-
 extern "C" int ekcg_gram_chunks(long long n, int d, int m1, int m2) {
     if (n < 1 || d < 1 || m1 < 1 || m2 < 1) return 1;
     return gram_chunks(n, d, m1, m2);
@@ -990,12 +883,12 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     if (vec4) {
         const dim3 g(chunks, d);
         switch (m1) {
-            case 4: launch_k(g_vec256 ? gemvt4_kernel<1, 4, true> : gemvt4_kernel<1, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 8: launch_k(g_vec256 ? gemvt4_kernel<2, 4, true> : gemvt4_kernel<2, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 16: launch_k(g_vec256 ? gemvt4_kernel<4, 4, true> : gemvt4_kernel<4, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 32: launch_k(g_vec256 ? gemvt4_kernel<8, 4, true> : gemvt4_kernel<8, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            case 64: launch_k(g_vec256 ? gemvt4_kernel<16, 4, true> : gemvt4_kernel<16, 4>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
-            default: launch_k(g_vec256 ? gemvt4_kernel<32, 2, true> : gemvt4_kernel<32, 2>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 4: launch_k(gemvt4_kernel<1, 4, true>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 8: launch_k(gemvt4_kernel<2, 4, true>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 16: launch_k(gemvt4_kernel<4, 4, true>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 32: launch_k(gemvt4_kernel<8, 4, true>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            case 64: launch_k(gemvt4_kernel<16, 4, true>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
+            default: launch_k(gemvt4_kernel<32, 2, true>, g, 256, 0, st, Xs, ldx, d, Y, n, rc, partials, live); break;
         }
     } else if (fn != nullptr && launch_gram_wide(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, gb, partials, live, st) == EKCG_OK) {
         // streamed (TMA bulk) Gram for 32-column blocks, stream_wide.cu
@@ -1035,23 +928,23 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
                       ((reinterpret_cast<uintptr_t>(Wout) | reinterpret_cast<uintptr_t>(beta != 0.0 ? Win : Wout)) % 16 == 0);
     auto grid_rows = [&](int rows_per_warp) {
         long long tiles = (n + rows_per_warp - 1) / rows_per_warp;
-        return grid_for(tiles, 4, 148LL * 16);
+        return grid_for(tiles, 4, (long long)device_sms() * 16);
     };
     if (launch_update_stream(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo, m2, beta, sign, n, live, st) == EKCG_OK) {
         // streamed (TMA bulk) update, stream.cu
     } else if (launch_update_wide_any(Qs, ldq, d, m1, C, Win, ldwi, Wout, ldwo, m2, beta, sign, n, live, st) == EKCG_OK) {
         // streamed update for 32 / 64-column blocks, stream_wide.cu
     } else if (m1 == m2 && even && m1 == 8) {
-        launch_k(g_upd_il ? update_dmma_kernel<8, 4, true> : update_dmma_kernel<8, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        launch_k(update_dmma_kernel<8, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                   sign, n, live);
     } else if (m1 == m2 && even && m1 == 16) {
-        launch_k(g_upd_il ? update_dmma_kernel<16, 4, true> : update_dmma_kernel<16, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
+        launch_k(update_dmma_kernel<16, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
     } else if (m1 == m2 && even && (m1 == 32 || m1 == 64) && (size_t)d * m1 * (m1 + 4) * 8 <= 200 * 1024) {
         const size_t smem = (size_t)d * m1 * (m1 + 4) * sizeof(double);
         const int mr = (m1 == 32) ? 4 : 2;
         long long tiles = (n + 8 * mr - 1) / (8 * mr);
-        unsigned grid = grid_for(tiles, 8, 148LL * 8);
+        unsigned grid = grid_for(tiles, 8, (long long)device_sms() * 8);
         if (m1 == 32) {
             auto fn = update_smem_kernel<32, 4>;
             cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1080,10 +973,10 @@ extern "C" int ekcg_tri_apply(const double* const* Ws, int ldw, const double* S,
     if (m < 1 || ldw < m || ldo < m || n < 0) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
     const bool even = (ldw % 2 == 0) && (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-    if (m == 64 && even && g_tri_skip) {
+    if (m == 64 && even) {
         const size_t smem = (size_t)64 * (64 + 4) * sizeof(double);
         long long tiles = (n + 15) / 16;
-        unsigned grid = grid_for(tiles, 8, 148LL * 8);
+        unsigned grid = grid_for(tiles, 8, (long long)device_sms() * 8);
         auto fn = update_smem_kernel<64, 2, true>;
         cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         launch_k(fn, grid, 256, smem, as_stream(stream), Ws, ldw, 1, S, (const double*)nullptr, m, out, ldo, 0.0, 1.0,
@@ -1110,7 +1003,7 @@ extern "C" int ekcg_xr_update(const double* W, int ldw, const double* AW, int ld
                      rho2_partials, live))
     const bool al = (ldw % 2 == 0) && (ldaw % 2 == 0) && ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(AW) |
                                                            reinterpret_cast<uintptr_t>(alpha)) % 16 == 0);
-    const bool al32 = g_vec256 && ldw % 4 == 0 && ldaw % 4 == 0 &&
+    const bool al32 = ldw % 4 == 0 && ldaw % 4 == 0 &&
                       ((reinterpret_cast<uintptr_t>(W) | reinterpret_cast<uintptr_t>(AW)) % 32 == 0);
     if (al && m == 64) XR4_LAUNCH(16);
     else if (al && m == 32) XR4_LAUNCH(8);

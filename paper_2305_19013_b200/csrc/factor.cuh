@@ -236,10 +236,12 @@ __device__ inline void finish_body(EkcgCtrl* ctrl, double rho2, int k, int kmax,
         ctrl->live = 0;
         return;
     }
-    if (!(rho > ctrl->tol_abs)) {
+    if (rho <= ctrl->tol_abs) {
         ctrl->status = 1;
         ctrl->live = 0;
-    } else if (k + 1 > kmax) {
+    } else if (!(rho > ctrl->tol_abs) || k + 1 > kmax) {
+        // NaN residual: the reference's loop test `history[-1] > tol * rho0` is false, so it stops, and
+        // `history[-1] <= tol * rho0` is false too, so the status is "maxiter" (solvers.py:357,417)
         ctrl->status = 2;
         ctrl->live = 0;
     }

@@ -16,21 +16,6 @@
 // per row (one per column group) and R rows per block, grid-striding over
 // rows -- no 64-bit integer division in the index math.
 // ---------------------------------------------------------------------------
-int g_csr_vec = 3;  // ekcg_tune key 17: CSR SpMM kernel choice (3: software-pipelined for m = 16 / 32 / 64 / 128,
-                    // else 1; 1: vectorized; 2: at most 2 columns per thread; 0: one thread per (row, column))
-
-int g_csr_w256 = 1;  // ekcg_tune key 22: 256-bit X gathers / Y stores in the pipelined CSR kernel when 32-B aligned
-
-static int sm_count() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        sms = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
-
 struct RowLaunch {
     dim3 grid, block;
 };
@@ -40,7 +25,7 @@ static RowLaunch row_launch(long long n, int groups) {
     int rows = 256 / groups;
     if (rows < 1) rows = 1;
     long long blocks = (n + rows - 1) / rows;
-    long long cap = 148LL * 16;
+    long long cap = (long long)device_sms() * 16;
     if (blocks > cap) blocks = cap;
     if (blocks < 1) blocks = 1;
     return {dim3((unsigned)blocks), dim3(groups, rows)};
@@ -379,14 +364,11 @@ csr_spmm_pf_kernel(const long long* __restrict__ rp, const int* __restrict__ ci,
 template <int G, bool W256>
 static void launch_csr_pf(const long long* rp, const int* ci, const double* vv, const double* X, int ldx, double* Y,
                           int ldy, long long n, const int* live, cudaStream_t st) {
-    static int occ = 0;
-    if (occ == 0 && (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, csr_spmm_pf_kernel<G, W256>, 256, 0) !=
-                         cudaSuccess || occ < 1)) {
-        cudaGetLastError();
-        occ = 1;
-    }
+    static int cache[kEkcgMaxDevices];
+    int occ = kernel_occupancy(csr_spmm_pf_kernel<G, W256>, 256, 0, cache);
+    if (occ < 1) occ = 1;
     constexpr int R = 256 / G;
-    long long blocks = (n + R - 1) / R, cap = (long long)occ * sm_count();
+    long long blocks = (n + R - 1) / R, cap = (long long)occ * device_sms();
     if (blocks > cap) blocks = cap;
     launch_k(csr_spmm_pf_kernel<G, W256>, dim3((unsigned)blocks), dim3(G, R), 0, st, rp, ci, vv, X, ldx, Y, ldy, n, live);
 }
@@ -461,19 +443,27 @@ extern "C" int ekcg_axpy_cols(double* W, int ldw, const double* Wprev, int ldp, 
     return launch_status();
 }
 
-extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const double* values,
-                             const double* X, int ldx, double* Y, int ldy, long long n, int m,
-                             const int* live, void* stream) {
-    if (n < 0 || m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
+// CSR kernel forms (ekcg_spmm_csr_kernel): every form computes each row as p0 + pairwise(p1..pk) with
+// separately rounded products, so they agree bit for bit; the automatic choice is the fastest that applies.
+enum CsrForm { kCsrAuto = 0, kCsrPipelined = 1, kCsrPipelined128 = 2, kCsrVec4 = 3, kCsrVec2 = 4, kCsrScalar = 5 };
+
+static int spmm_csr_impl(int form, const long long* row_ptr, const int* col_idx, const double* values,
+                         const double* X, int ldx, double* Y, int ldy, long long n, int m, const int* live,
+                         cudaStream_t st) {
+    if (n < 0 || m < 1 || ldx < m || ldy < m || form < kCsrAuto || form > kCsrScalar) return EKCG_EINVAL;
     if (n == 0) return EKCG_OK;
-    cudaStream_t st = as_stream(stream);
     const bool al16 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 15) == 0 &&
                       ldx % 2 == 0 && ldy % 2 == 0;
+    const bool al32 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 31) == 0 &&
+                      ldx % 4 == 0 && ldy % 4 == 0;
     const int G = m / 4;
-    if (g_csr_vec == 3 && m % 4 == 0 && (G == 4 || G == 8 || G == 16 || G == 32) && al16) {
-        const bool al32 = ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 31) == 0 &&
-                          ldx % 4 == 0 && ldy % 4 == 0 && g_csr_w256;
-        if (al32) {
+    const bool pf_ok = m % 4 == 0 && (G == 4 || G == 8 || G == 16 || G == 32) && al16;
+    const bool v4_ok = m % 4 == 0 && m / 4 <= 256 && al16;
+    const bool v2_ok = m % 2 == 0 && m / 2 <= 256 && al16;
+    if (form == kCsrAuto) form = pf_ok ? kCsrPipelined : v4_ok ? kCsrVec4 : v2_ok ? kCsrVec2 : kCsrScalar;
+    if (form == kCsrPipelined || form == kCsrPipelined128) {
+        if (!pf_ok) return EKCG_EINVAL;
+        if (form == kCsrPipelined && al32) {  // 256-bit X gathers / Y stores
             if (G == 4) launch_csr_pf<4, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
             else if (G == 8) launch_csr_pf<8, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
             else if (G == 16) launch_csr_pf<16, true>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
@@ -484,13 +474,15 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
             else if (G == 16) launch_csr_pf<16, false>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
             else launch_csr_pf<32, false>(row_ptr, col_idx, values, X, ldx, Y, ldy, n, live, st);
         }
-    } else if (g_csr_vec && g_csr_vec != 2 && m % 4 == 0 && m / 4 <= 256 && al16) {
+    } else if (form == kCsrVec4) {
+        if (!v4_ok) return EKCG_EINVAL;
         RowLaunch L = row_launch(n, m / 4);
         launch_k(csr_spmm_vec_kernel<4>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
-    } else if (g_csr_vec && m % 2 == 0 && m / 2 <= 256 && al16) {
+    } else if (form == kCsrVec2) {
+        if (!v2_ok) return EKCG_EINVAL;
         RowLaunch L = row_launch(n, m / 2);
         launch_k(csr_spmm_vec_kernel<2>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
-    } else if (g_csr_vec && m == 1) {
+    } else if (m == 1) {
         RowLaunch L = row_launch(n, 1);
         launch_k(csr_spmm_vec_kernel<1>, L.grid, L.block, 0, st, row_ptr, col_idx, values, X, ldx, Y, ldy, n, live);
     } else {
@@ -501,21 +493,39 @@ extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const
     return launch_status();
 }
 
-extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
-                                 int m, const int* live, void* stream) {
-    if (m < 1 || ldx < m || ldy < m) return EKCG_EINVAL;
+extern "C" int ekcg_spmm_csr(const long long* row_ptr, const int* col_idx, const double* values,
+                             const double* X, int ldx, double* Y, int ldy, long long n, int m,
+                             const int* live, void* stream) {
+    return spmm_csr_impl(kCsrAuto, row_ptr, col_idx, values, X, ldx, Y, ldy, n, m, live, as_stream(stream));
+}
+
+extern "C" int ekcg_spmm_csr_kernel(int form, const long long* row_ptr, const int* col_idx, const double* values,
+                                    const double* X, int ldx, double* Y, int ldy, long long n, int m,
+                                    const int* live, void* stream) {
+    return spmm_csr_impl(form, row_ptr, col_idx, values, X, ldx, Y, ldy, n, m, live, as_stream(stream));
+}
+
+// Stencil kernel forms (ekcg_spmm_stencil_kernel): 0 automatic (the TMA plane march above
+// kMarchMinWork block entries, else the row-parallel kernel), 1 the plane march at any size, 2 the
+// row-parallel kernel.  Both kernels reproduce the generator's CSR association, so they agree bit for bit.
+static int spmm_stencil_impl(int form, const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
+                             int m, const int* live, cudaStream_t st) {
+    if (m < 1 || ldx < m || ldy < m || form < 0 || form > 2) return EKCG_EINVAL;
     EkcgStencil s;
     UniformFaces uf;
     long long n;
     int rc = prepare_stencil(desc, s, uf, n);
     if (rc != EKCG_OK) return rc;
-    cudaStream_t st = as_stream(stream);
     const bool aligned = (ldx % 2 == 0) && (ldy % 2 == 0) && ((reinterpret_cast<uintptr_t>(X) & 15) == 0) &&
                          ((reinterpret_cast<uintptr_t>(Y) & 15) == 0);
     n = s.row_end - s.row_begin;
-    if (g_stencil_march && launch_stencil_march(s, uf, X, ldx, Y, ldy, m, live, st) == EKCG_OK) {
-        ++g_ekcg_launches;
-        return launch_status();
+    if (form != 2) {
+        const long long min_work = form == 1 ? 0 : kMarchMinWork;
+        if (launch_stencil_march(s, uf, X, ldx, Y, ldy, m, live, st, min_work) == EKCG_OK) {
+            ++g_ekcg_launches;
+            return launch_status();
+        }
+        if (form == 1) return EKCG_EINVAL;
     }
     if (aligned && m % 4 == 0) {
         RowLaunch L = row_launch(n, m / 4);
@@ -529,4 +539,14 @@ extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int l
     }
     ++g_ekcg_launches;
     return launch_status();
+}
+
+extern "C" int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
+                                 int m, const int* live, void* stream) {
+    return spmm_stencil_impl(0, desc, X, ldx, Y, ldy, m, live, as_stream(stream));
+}
+
+extern "C" int ekcg_spmm_stencil_kernel(int form, const EkcgStencil* desc, const double* X, int ldx, double* Y,
+                                        int ldy, int m, const int* live, void* stream) {
+    return spmm_stencil_impl(form, desc, X, ldx, Y, ldy, m, live, as_stream(stream));
 }

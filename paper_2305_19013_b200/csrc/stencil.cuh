@@ -262,15 +262,13 @@ static inline int prepare_stencil(const EkcgStencil* desc, EkcgStencil& s, Unifo
     return EKCG_OK;
 }
 
-// Plane-marching stencil SpMM (stencil_march.cu); EKCG_EINVAL when it does not apply.
+// Below this many block entries (rows x columns) the row-parallel kernels finish sooner than the
+// plane march, which is latency-bound on small grids (a few CTAs, serial plane steps).
+constexpr long long kMarchMinWork = 1LL << 21;
+// Plane-marching stencil SpMM (stencil_march.cu) over at least min_work block entries; EKCG_EINVAL when it
+// does not apply.
 int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy,
-                     int m, const int* live, cudaStream_t st);
-extern int g_stencil_march;  // ekcg_tune key 3
-extern int g_march_variant;  // ekcg_tune key 4
-extern int g_march_fused;    // ekcg_tune key 9
-extern int g_fused_variant;  // ekcg_tune key 13
-// below this many block entries (rows x columns) the row-parallel kernels win (ekcg_tune key 12)
-extern long long g_march_min_work;
+                         int m, const int* live, cudaStream_t st, long long min_work);
 // Fused plane-marching kernels for m = 16 (stencil_march.cu); EKCG_EINVAL when they do not apply.
 int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, int m,
                          double* partials, unsigned int* counter, double* S, EkcgCtrl* ctrl, int iteration, double tol,

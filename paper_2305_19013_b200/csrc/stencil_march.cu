@@ -267,20 +267,10 @@ int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, 
     CUtensorMap map;
     if (!make_plane_map<P>(s, X, ldx, m, map)) return EKCG_EINVAL;
 
-    static int resident = 0;
-    if (resident == 0) {
-        cudaFuncSetAttribute(stencil_march_kernel<P>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)P::SMEM);
-        int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, stencil_march_kernel<P>, P::NT, P::SMEM) !=
-                cudaSuccess || occ < 1) {
-            cudaGetLastError();
-            occ = 1;
-        }
-        int dev = 0, sms = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        resident = occ * sms;
-    }
+    static int cache[kEkcgMaxDevices];
+    const int occ = kernel_occupancy(stencil_march_kernel<P>, P::NT, P::SMEM, cache);
+    if (occ < 1) return EKCG_EINVAL;
+    const long long resident = (long long)occ * device_sms();
     const long long tiles = (DIM == 3) ? (long long)((s.nx + P::TX - 1) / P::TX) * ((s.ny + P::TY - 1) / P::TY)
                                        : (long long)((s.nx + P::TX - 1) / P::TX);
     const int colchunks = (m + KC - 1) / KC;
@@ -540,22 +530,10 @@ int launch_march_fused(const EkcgStencil& s, const UniformFaces& uf, const doubl
     if (!make_plane_map<P>(s, X, 16, 16, map)) return EKCG_EINVAL;
     constexpr size_t smem = P::SMEM + sizeof(double) * 64 * 16;
     static_assert(P::SMEM >= sizeof(double) * 11 * 256, "reduction scratch fits the stages");
-    static int resident = 0;
-    if (resident == 0) {
-        auto fn = stencil_march_fused_kernel<P, EPI>;
-        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) {
-            cudaGetLastError();
-            return EKCG_EINVAL;
-        }
-        int occ = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, P::NT, smem) != cudaSuccess || occ < 1) {
-            cudaGetLastError();
-            occ = 1;
-        }
-        int dev = 0, sms = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        resident = occ * sms;
-    }
+    static int cache[kEkcgMaxDevices];
+    const int occ = kernel_occupancy(stencil_march_fused_kernel<P, EPI>, P::NT, smem, cache);
+    if (occ < 1) return EKCG_EINVAL;
+    const long long resident = (long long)occ * device_sms();
     const long long tiles = (DIM == 3) ? (long long)((s.nx + P::TX - 1) / P::TX) * ((s.ny + P::TY - 1) / P::TY)
                                        : (long long)((s.nx + P::TX - 1) / P::TX);
     int grid = resident < max_ctas ? resident : max_ctas;
@@ -578,7 +556,7 @@ int launch_march_fused(const EkcgStencil& s, const UniformFaces& uf, const doubl
 // aligned rows, whole planes in the row range); EKCG_EINVAL otherwise, and
 // the caller takes the row-parallel kernel.
 int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, double* Y, int ldy,
-                         int m, const int* live, cudaStream_t st) {
+                         int m, const int* live, cudaStream_t st, long long min_work) {
     if (m % 4 != 0 || ldx % 2 != 0 || ldy % 2 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) ||
         (reinterpret_cast<uintptr_t>(Y) & 15))
         return EKCG_EINVAL;
@@ -586,21 +564,11 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
     if (s.row_begin % plane != 0 || s.row_end % plane != 0) return EKCG_EINVAL;
     // small grids: the march is latency-bound (a few CTAs, serial plane steps);
     // the row-parallel kernel finishes sooner
-    if ((s.row_end - s.row_begin) * (long long)m < g_march_min_work) return EKCG_EINVAL;
+    if ((s.row_end - s.row_begin) * (long long)m < min_work) return EKCG_EINVAL;
     const int wb = (int)(s.row_begin / plane), we = (int)(s.row_end / plane);
     const int kc = (m % 16 == 0) ? 16 : (m % 8 == 0) ? 8 : 4;
     if (s.dim == 3) {
-        if (kc == 16) {
-            switch (g_march_variant) {
-                case 1: return launch_march<March<3, 16, 16, 8, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                case 2: return launch_march<March<3, 16, 16, 4, 8>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                case 3: return launch_march<March<3, 16, 32, 4, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                case 4: return launch_march<March<3, 16, 16, 4, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                case 5: return launch_march<March<3, 16, 16, 8, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                case 6: return launch_march<March<3, 16, 32, 8, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-                default: return launch_march<March<3, 16, 16, 4, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
-            }
-        }
+        if (kc == 16) return launch_march<March<3, 16, 16, 4, 4>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
         if (kc == 8) return launch_march<March<3, 8, 16, 8, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
         return launch_march<March<3, 4, 16, 16, 6>>(s, uf, X, ldx, Y, ldy, m, wb, we, live, st);
     }
@@ -610,15 +578,14 @@ int launch_stencil_march(const EkcgStencil& s, const UniformFaces& uf, const dou
 }
 
 // Fused plane-marching kernels for m = 16 (EKCG_EINVAL when they do not apply:
-// the caller takes the row-parallel fused kernels).
-int g_march_fused = 1;  // ekcg_tune key 9
-int g_fused_variant = 0;  // ekcg_tune key 13
+// the caller takes the row-parallel fused kernels).  Gram partials reduced in
+// groups of 3 CTAs, 2 levels (tools/kernel_times.py --fused).
 
 int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const double* X, int ldx, int m,
                          double* partials, unsigned int* counter, double* S, EkcgCtrl* ctrl, int iteration, double tol,
                          int finalize, int max_ctas, cudaStream_t st) {
-    if (!g_march_fused || m != 16 || ldx != 16 || (reinterpret_cast<uintptr_t>(X) & 15) ||
-        (s.row_end - s.row_begin) * 16 < g_march_min_work)
+    if (m != 16 || ldx != 16 || (reinterpret_cast<uintptr_t>(X) & 15) ||
+        (s.row_end - s.row_begin) * 16 < kMarchMinWork)
         return EKCG_EINVAL;
     FusedArgs fa{};
     fa.partials = partials;
@@ -628,17 +595,7 @@ int launch_march_cholinv(const EkcgStencil& s, const UniformFaces& uf, const dou
     fa.tol = tol;
     fa.finalize = finalize;
     fa.out = S;
-    if (s.dim == 3) {
-        switch (g_fused_variant) {
-            case 1: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
-            case 2: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
-            case 3: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 3, 2);
-            case 4: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 2, 4);
-            case 5: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 6, 2);
-            case 6: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 4, 1);
-            default: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 3, 2);
-        }
-    }
+    if (s.dim == 3) return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st, 3, 2);
     return launch_march_fused<March<2, 16, 64, 1, 4>, EPI_GRAM>(s, uf, X, max_ctas, fa, st);
 }
 
@@ -646,8 +603,8 @@ int launch_march_xr(const EkcgStencil& s, const UniformFaces& uf, const double* 
                     const double* alpha, double* x, double* r, double* partials, unsigned int* counter, EkcgCtrl* ctrl,
                     int k, int kmax, int stag, double* history, int do_finish, double* rho2_out, int max_ctas,
                     cudaStream_t st) {
-    if (!g_march_fused || m != 16 || ldx != 16 || ldy % 2 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) ||
-        (reinterpret_cast<uintptr_t>(Y) & 15) || (s.row_end - s.row_begin) * 16 < g_march_min_work)
+    if (m != 16 || ldx != 16 || ldy % 2 != 0 || (reinterpret_cast<uintptr_t>(X) & 15) ||
+        (reinterpret_cast<uintptr_t>(Y) & 15) || (s.row_end - s.row_begin) * 16 < kMarchMinWork)
         return EKCG_EINVAL;
     FusedArgs fa{};
     fa.partials = partials;
@@ -664,16 +621,6 @@ int launch_march_xr(const EkcgStencil& s, const UniformFaces& uf, const double* 
     fa.history = history;
     fa.do_finish = do_finish;
     fa.rho2_out = rho2_out;
-    if (s.dim == 3) {
-        switch (g_fused_variant) {
-            case 1: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_XR>(s, uf, X, max_ctas, fa, st);
-            case 2: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
-            case 3: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_XR>(s, uf, X, max_ctas, fa, st, 3, 2);
-            case 4: return launch_march_fused<March<3, 16, 16, 4, 6>, EPI_XR>(s, uf, X, max_ctas, fa, st, 2, 4);
-            case 5: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 6, 2);
-            case 6: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 4, 1);
-            default: return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 3, 2);
-        }
-    }
+    if (s.dim == 3) return launch_march_fused<March<3, 16, 16, 4, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st, 3, 2);
     return launch_march_fused<March<2, 16, 64, 1, 4>, EPI_XR>(s, uf, X, max_ctas, fa, st);
 }

@@ -139,35 +139,21 @@ gram16_stream_kernel(const double* const* __restrict__ Xs, int d, const double* 
 }
 
 template <int GB, int R, int NS>
+int gram16_stream_occupancy() {
+    static int cache[kEkcgMaxDevices];
+    return kernel_occupancy(gram16_stream_kernel<GB, R, NS>, 160, Gram16Stream<GB, R, NS>::SMEM, cache);
+}
+
+template <int GB, int R, int NS>
 int launch_gram16_stream(const double* const* Xs, int d, const double* Y, long long n, int chunks,
                          long long rows_chunk, double* partials, const int* live, cudaStream_t st) {
     using P = Gram16Stream<GB, R, NS>;
-    auto fn = gram16_stream_kernel<GB, R, NS>;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P::SMEM) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return EKCG_EINVAL;
-        }
-        attr = true;
-    }
+    if (gram16_stream_occupancy<GB, R, NS>() < 1) return EKCG_EINVAL;
     dim3 grid(chunks, (d + GB - 1) / GB);
-    launch_k(fn, grid, 160, P::SMEM, st, Xs, d, Y, n, rows_chunk, partials, live);
+    launch_k(gram16_stream_kernel<GB, R, NS>, grid, 160, P::SMEM, st, Xs, d, Y, n, rows_chunk, partials, live);
     return EKCG_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Streamed DMMA update for 16-column blocks:
-//   Wout = beta Win + sign sum_i Q_i C_i      (CGS2 projection removal)
-// Each CTA walks R-row slabs (grid-stride); per slab the producer streams
-// Q_0 .. Q_{d-1} row slabs through an NS-slot ring (1-D bulk copies).  Warp w
-// owns rows 16w .. 16w+15 of the slab (two 8-row DMMA tiles).  A fragments
-// come from shared memory "diagonally": load j of lane (row i, k) reads column
-// 4((j + i) mod 4) + k, so the 8 rows of a load hit 4 different bank groups
-// (no conflicts beyond the minimum), and k-step kk takes load (kk - i) mod 4.
-// B fragments (C_i) come through L1.  Win is read and Wout written with
-// 16-B accesses in the epilogue (in place allowed: same thread, same rows).
 // ---------------------------------------------------------------------------
 template <int R, int NS>
 __global__ void __launch_bounds__(160)
@@ -276,68 +262,50 @@ int launch_update16_stream(const double* const* Qs, int d, const double* C, cons
                            double beta, double sign, long long n, const int* live, cudaStream_t st) {
     auto fn = update16_stream_kernel<R, NS>;
     constexpr size_t smem = sizeof(double) * (R * 16 + 256) * NS;
-    static int grid = 0;
-    if (grid == 0) {
-        if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess) {
-            cudaGetLastError();
-            return EKCG_EINVAL;
-        }
-        int occ = 0, dev = 0, sms = 148;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 160, smem) != cudaSuccess || occ < 1) {
-            cudaGetLastError();
-            occ = 1;
-        }
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        grid = occ * sms;
-    }
+    static int cache[kEkcgMaxDevices];
+    const int occ = kernel_occupancy(fn, 160, smem, cache);
+    if (occ < 1) return EKCG_EINVAL;
+    const long long grid = (long long)occ * device_sms();
     const long long slabs = (n + R - 1) / R;
     const int g = (int)(slabs < grid ? slabs : grid);
     launch_k(fn, g, 160, smem, st, Qs, d, C, Win, Wout, beta, sign, n, live);
     return EKCG_OK;
 }
 
+// The ring shapes (measured on B200, tools/tune_gram.py, tools/dsweep.py): d = 1 Grams take one block per
+// CTA with 64-row slabs in 4 stages (3 CTAs per SM); longer histories 4 blocks per CTA sharing 48-row Y
+// slabs in 3 stages (2 CTAs per SM); updates 64-row Q slabs in 6 stages (3 CTAs per SM).
+constexpr int kGramD1GB = 1, kGramD1R = 64, kGramD1NS = 4;
+constexpr int kGramGB = 4, kGramR = 48, kGramNS = 3;
+constexpr int kUpdR = 64, kUpdNS = 6;
+
 }  // namespace
 
-int g_gram_stream = 10;  // ekcg_tune key 7: streamed Gram for 16-column blocks, 0 off, 1.. variants
-int g_gram16_d1 = 1;    // ekcg_tune key 21: one-block (d = 1) streamed Gram with GB = 1 (3 CTAs per SM)
+// Co-resident CTAs of the streamed m = 16 Gram that ekcg_gram launches for d blocks (the chunking fills whole
+// waves of exactly this kernel instance; 0 when it cannot launch here).
+int gram16_stream_slots(int d) {
+    const int occ = d == 1 ? gram16_stream_occupancy<kGramD1GB, kGramD1R, kGramD1NS>()
+                           : gram16_stream_occupancy<kGramGB, kGramR, kGramNS>();
+    return occ * device_sms();
+}
 
 // Streamed Gram when it applies (16 contiguous columns, aligned); EKCG_EINVAL otherwise.
 int launch_gram_stream(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
                        int chunks, long long rows_chunk, double* partials, const int* live, cudaStream_t st) {
-    if (!g_gram_stream || m1 != 16 || m2 != 16 || ldx != 16 || ldy != 16 || (reinterpret_cast<uintptr_t>(Y) & 15) ||
+    if (m1 != 16 || m2 != 16 || ldx != 16 || ldy != 16 || (reinterpret_cast<uintptr_t>(Y) & 15) ||
         rows_chunk % 16 != 0)
         return EKCG_EINVAL;
-    if (d == 1 && g_gram16_d1) return launch_gram16_stream<1, 64, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-    switch (g_gram_stream) {
-        case 2: return launch_gram16_stream<4, 32, 6>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 3: return launch_gram16_stream<4, 64, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 4: return launch_gram16_stream<2, 64, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 5: return launch_gram16_stream<4, 64, 3>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 6: return launch_gram16_stream<2, 128, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 7: return launch_gram16_stream<8, 32, 5>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 8: return launch_gram16_stream<4, 48, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 9: return launch_gram16_stream<4, 32, 5>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        case 10: return launch_gram16_stream<4, 48, 3>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-        default: return launch_gram16_stream<4, 32, 4>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
-    }
+    if (d == 1)
+        return launch_gram16_stream<kGramD1GB, kGramD1R, kGramD1NS>(Xs, d, Y, n, chunks, rows_chunk, partials, live,
+                                                                    st);
+    return launch_gram16_stream<kGramGB, kGramR, kGramNS>(Xs, d, Y, n, chunks, rows_chunk, partials, live, st);
 }
-
-int g_update_stream = 5;  // ekcg_tune key 8: streamed update for 16-column blocks, 0 off, 1.. variants
 
 int launch_update_stream(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
                          double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                          cudaStream_t st) {
-    if (!g_update_stream || m1 != 16 || m2 != 16 || ldq != 16 || ldwo != 16 || (beta != 0.0 && ldwi != 16) ||
+    if (m1 != 16 || m2 != 16 || ldq != 16 || ldwo != 16 || (beta != 0.0 && ldwi != 16) ||
         ((reinterpret_cast<uintptr_t>(Wout) | reinterpret_cast<uintptr_t>(beta != 0.0 ? Win : Wout)) & 15))
         return EKCG_EINVAL;
-    switch (g_update_stream) {
-        case 2: return launch_update16_stream<64, 8>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-        case 3: return launch_update16_stream<128, 8>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-        case 4: return launch_update16_stream<32, 16>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-        case 5: return launch_update16_stream<64, 6>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-        case 6: return launch_update16_stream<64, 10>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-        case 7: return launch_update16_stream<32, 12>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-        default: return launch_update16_stream<64, 12>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
-    }
+    return launch_update16_stream<kUpdR, kUpdNS>(Qs, d, C, Win, Wout, beta, sign, n, live, st);
 }

@@ -312,16 +312,6 @@ int resident_ctas(K fn, size_t smem, int threads = 160) {
     return occ;
 }
 
-int num_sms() {
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        sms = 148;
-        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return sms;
-}
-
 template <int M, int MR, int NS, int CW>
 int launch_update_wide(const double* const* Qs, int d, const double* C, const double* Win, int ldwi, double* Wout,
                        int ldwo, double beta, double sign, long long n, const int* live, cudaStream_t st) {
@@ -332,16 +322,13 @@ int launch_update_wide(const double* const* Qs, int d, const double* C, const do
     const int occ = resident_ctas(fn, smem, 32 * (CW + 1));
     if (occ < 1) return EKCG_EINVAL;
     const long long slabs = (n + P::R - 1) / P::R;
-    const long long slots = (long long)occ * num_sms();
+    const long long slots = (long long)occ * device_sms();
     const int g = (int)(slabs < slots ? slabs : slots);
     launch_k(fn, g, 32 * (CW + 1), smem, st, Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live);
     return EKCG_OK;
 }
 
 }  // namespace
-
-int g_wide_stream = 1;  // ekcg_tune key 15: streamed wide-block (m = 32 / 64) Gram and update, 0 off
-int g_wide_upd_variant = 0;  // ekcg_tune key 16
 
 // Rows per Gram step (R) and resident CTAs of the m = 32 streamed Gram.
 constexpr int kGram32R = 32, kGram32NS = 4;
@@ -350,13 +337,13 @@ int gram_wide_slots(int gb) {
     size_t smem = gb == 2 ? GramWide<32, 2, kGram32R, kGram32NS>::SMEM : GramWide<32, 1, kGram32R, kGram32NS>::SMEM;
     int occ = gb == 2 ? resident_ctas(gram_wide_stream_kernel<32, 2, kGram32R, kGram32NS>, smem)
                       : resident_ctas(gram_wide_stream_kernel<32, 1, kGram32R, kGram32NS>, smem);
-    return (occ < 1 ? 1 : occ) * num_sms();
+    return (occ < 1 ? 1 : occ) * device_sms();
 }
 
 // Streamed Gram for 32 contiguous columns (aligned); EKCG_EINVAL otherwise.
 int launch_gram_wide(const double* const* Xs, int ldx, int d, int m1, const double* Y, int ldy, int m2, long long n,
                      int chunks, long long rows_chunk, int gb, double* partials, const int* live, cudaStream_t st) {
-    if (!g_wide_stream || m1 != 32 || m2 != 32 || ldx != 32 || ldy != 32 || (reinterpret_cast<uintptr_t>(Y) & 15) ||
+    if (m1 != 32 || m2 != 32 || ldx != 32 || ldy != 32 || (reinterpret_cast<uintptr_t>(Y) & 15) ||
         rows_chunk % 16 != 0 || (gb != 1 && gb != 2))
         return EKCG_EINVAL;
     dim3 grid(chunks, (d + gb - 1) / gb);
@@ -374,29 +361,16 @@ int launch_gram_wide(const double* const* Xs, int ldx, int d, int m1, const doub
     return EKCG_OK;
 }
 
-// Streamed update for 32 / 64 contiguous columns (aligned rows); EKCG_EINVAL
+// Streamed update for 32 contiguous columns (aligned rows); EKCG_EINVAL
 // when it does not apply or C_i do not fit in shared memory.
 int launch_update_wide_any(const double* const* Qs, int ldq, int d, int m1, const double* C, const double* Win, int ldwi,
                            double* Wout, int ldwo, int m2, double beta, double sign, long long n, const int* live,
                            cudaStream_t st) {
-    if (!g_wide_stream || m1 != m2 || (m1 != 32 && m1 != 64) || ldq != m1 || ldwo % 2 != 0 ||
-        (beta != 0.0 && ldwi % 2 != 0) ||
+    if (m1 != 32 || m2 != 32 || ldq != 32 || ldwo % 2 != 0 || (beta != 0.0 && ldwi % 2 != 0) ||
         ((reinterpret_cast<uintptr_t>(Wout) | reinterpret_cast<uintptr_t>(beta != 0.0 ? Win : Wout)) & 15))
         return EKCG_EINVAL;
-    // variants (ekcg_tune key 16), m = 32: 0 = 8 consumer warps x 1 tile (default), 1 = 4 x 2, 2 = 8 x 2
-    const int v = g_wide_upd_variant;
-    int rc = EKCG_EINVAL;
-    if (m1 == 32) {
-        if (v == 1) rc = launch_update_wide<32, 2, 4, 4>(Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live, st);
-        else if (v == 2) rc = launch_update_wide<32, 2, 3, 8>(Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live, st);
-        else rc = launch_update_wide<32, 1, 4, 8>(Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live, st);
-        return rc;
-    }
-    // m = 64: the register-direct smem-C kernel (dense.cu) measured faster at
-    // d = 2, 3 (29.8 vs 24.1 TFLOP/s at d = 3, tools/kernel_times.py --wide):
-    // the 64 x 64 C_i leave room for too few ring slots and warps.  The
-    // streamed variants stay selectable for A/B runs and tests.
-    if (v == 1) rc = launch_update_wide<64, 2, 3, 4>(Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live, st);
-    else if (v == 2) rc = launch_update_wide<64, 1, 2, 8>(Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live, st);
-    return rc;
+    // m = 32: 8 consumer warps x 1 tile over a 4-stage Q-slab ring (tools/kernel_times.py --wide).  At m = 64 the
+    // register-direct smem-C kernel (dense.cu) is faster (29.8 vs 24.1 TFLOP/s at d = 3): the 64 x 64 C_i leave
+    // room for too few ring slots and warps, so the streamed m = 64 variants were dropped.
+    return launch_update_wide<32, 1, 4, 8>(Qs, d, C, Win, ldwi, Wout, ldwo, beta, sign, n, live, st);
 }

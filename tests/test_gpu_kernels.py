@@ -57,9 +57,9 @@ def test_csr_spmm_bitwise(kernels_golden, tag):
 
 @pytest.mark.parametrize("m", [1, 2, 4, 6, 12, 32, 64])
 def test_csr_vectorized_equals_scalar_kernel(m):
-    """The vectorized CSR kernel (ekcg_tune 17) against the one-thread-per-(row, column)
-    kernel, bitwise, on rows of 1..20 entries (the < 8 fast path, the 8 / 9 boundary
-    and the pairwise tail)."""
+    """Every CSR kernel form (ekcg_spmm_csr_kernel: 4 / 2 columns per thread, one thread
+    per (row, column), the automatic choice) bitwise, on rows of 1..20 entries (the < 8
+    fast path, the 8 / 9 boundary and the pairwise tail)."""
     rng = np.random.default_rng(m)
     n = 5000
     lens = rng.integers(1, 21, n)
@@ -70,24 +70,24 @@ def test_csr_vectorized_equals_scalar_kernel(m):
     X = dev(rng.standard_normal((n, m)))
     rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
     outs = []
-    for vec in (1, 2, 0, 3):
-        _lib.call("ekcg_tune", 17, vec)
-        Y = torch.empty_like(X)
-        _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(), m, Y.data_ptr(),
-                  m, n, m, None, stream())
+    for form in (3, 4, 5, 0):
+        Y = torch.full_like(X, float("nan"))
+        rc = _lib.query("ekcg_spmm_csr_kernel", form, rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(),
+                        m, Y.data_ptr(), m, n, m, None, stream())
+        if rc != 0:  # the form does not apply to this width
+            assert (form == 3 and m % 4) or (form == 4 and m % 2), (form, m, rc)
+            continue
         outs.append(Y.cpu().numpy())
-    _lib.call("ekcg_tune", 17, 3)  # back to the default
-    assert np.array_equal(outs[0].view(np.int64), outs[2].view(np.int64))
-    assert np.array_equal(outs[1].view(np.int64), outs[2].view(np.int64))
-    assert np.array_equal(outs[3].view(np.int64), outs[2].view(np.int64))
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.int64), outs[0].view(np.int64))
     ref = orc.csr_spmm(rp, ci.astype(np.int64), vals, X.cpu().numpy())
     assert np.array_equal(outs[0].view(np.int64), ref.view(np.int64))
 
 
 @pytest.mark.parametrize("m", [16, 32, 64, 128])
 def test_csr_pipelined_equals_vectorized(m):
-    """The software-pipelined CSR kernel (ekcg_tune 17 = 3) against the vectorized
-    one, bitwise, with enough rows that every thread walks several rows (the
+    """The software-pipelined CSR kernel (256-bit and 128-bit accesses) against the
+    vectorized one, bitwise, with enough rows that every thread walks several rows (the
     pipelined pairs / row pointers), rows of 1..20 entries and a ragged last warp."""
     rng = np.random.default_rng(100 + m)
     n = 300_001 if m <= 32 else 100_003
@@ -99,21 +99,13 @@ def test_csr_pipelined_equals_vectorized(m):
     X = dev(rng.standard_normal((n, m)))
     rp_d, ci_d, v_d = dev(rp, torch.int64), dev(ci, torch.int32), dev(vals)
     outs = []
-    for vec, w256 in ((3, 1), (1, 1), (3, 0)):  # pipelined with 256-bit / 128-bit accesses, vectorized
-        _lib.call("ekcg_tune", 17, vec)
-        _lib.call("ekcg_tune", 22, w256)
+    for form in (1, 3, 2):  # pipelined with 256-bit / 128-bit accesses, vectorized
         Y = torch.full_like(X, float("nan"))
-        _lib.call("ekcg_spmm_csr", rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(), X.data_ptr(), m, Y.data_ptr(),
-                  m, n, m, None, stream())
+        assert _lib.query("ekcg_spmm_csr_kernel", form, rp_d.data_ptr(), ci_d.data_ptr(), v_d.data_ptr(),
+                          X.data_ptr(), m, Y.data_ptr(), m, n, m, None, stream()) == 0
         outs.append(Y.cpu().numpy())
-    _lib.call("ekcg_tune", 17, 3)  # back to the defaults
-    _lib.call("ekcg_tune", 22, 1)
     assert np.array_equal(outs[0].view(np.int64), outs[1].view(np.int64))
     assert np.array_equal(outs[2].view(np.int64), outs[1].view(np.int64))
-    rows = np.arange(0, n, 997)
-    sub = orc.csr_spmm(rp, ci.astype(np.int64), vals, X.cpu().numpy())[rows]
-    assert np.array_equal(outs[0][rows].view(np.int64), sub.view(np.int64))
-
 
 
 @pytest.mark.parametrize("shift", [0, 2, 1])
@@ -166,11 +158,8 @@ def test_march_tile_field_bitwise(idx, edge, m):
     X = np.random.default_rng(idx + edge + m).standard_normal((prob.n, m))
     Xd = dev(X)
     Yd = torch.empty_like(Xd)
-    assert _lib.query("ekcg_tune", 12, 0) == 0  # march kernel at any size
-    try:
-        op.apply(Xd, m, Yd, m, m)
-    finally:
-        _lib.call("ekcg_tune", 12, 1 << 21)
+    assert _lib.query("ekcg_spmm_stencil_kernel", 1, op.desc_ref(), Xd.data_ptr(), m, Yd.data_ptr(), m, m, None,
+                      stream()) == 0  # the plane march at any size
     ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, X)
     assert np.array_equal(Yd.cpu().numpy().view(np.int64), ref.view(np.int64))
 
@@ -179,7 +168,7 @@ def test_march_tile_field_bitwise(idx, edge, m):
                                          ((2, 2, 2), None), ((130, 7), "node"), ((21, 19, 11), "node")])
 @pytest.mark.parametrize("m", [4, 12, 16, 20, 64])
 def test_stencil_march_kernel(shape, kappa, m):
-    """Plane-marching kernel (ekcg_tune key 3) vs the row kernel vs the CSR oracle,
+    """Plane-marching kernel (form 1) vs the row kernel (form 2) vs the CSR oracle,
     on ragged tiles, partial column chunks and plane-aligned row ranges."""
     import ctypes
     rng = np.random.default_rng(len(shape) * 1000 + m + shape[0])
@@ -198,27 +187,24 @@ def test_stencil_march_kernel(shape, kappa, m):
     ref = orc.csr_spmm(A.row_ptr, A.col_idx, A.values, X)
     Xd = dev(X)
     outs = []
-    assert _lib.query("ekcg_tune", 12, 0) == 0  # march kernel at any size
-    try:
-        for march in (1, 0):
-            assert _lib.query("ekcg_tune", 3, march) == 0
-            Yd = torch.full_like(Xd, np.nan)
-            op.apply(Xd, m, Yd, m, m)
-            outs.append(Yd.cpu().numpy())
-        # plane-aligned row range (one shard's slab), march on
-        assert _lib.query("ekcg_tune", 3, 1) == 0
-        plane = n // shape[-1]
-        lo, hi = plane * (shape[-1] // 3), plane * max(shape[-1] // 3 + 1, (2 * shape[-1]) // 3)
-        d = op._desc
-        sub = type(d)()
-        ctypes.pointer(sub)[0] = d
-        sub.row_begin, sub.row_end = lo, hi
+    for form in (1, 2):  # plane march at any size, row-parallel kernel
         Yd = torch.full_like(Xd, np.nan)
+        rc = _lib.query("ekcg_spmm_stencil_kernel", form, op.desc_ref(), Xd.data_ptr(), m, Yd.data_ptr(), m, m,
+                        None, stream())
+        assert rc == 0 or (form == 1 and m % 4), (form, m, rc)
+        outs.append(Yd.cpu().numpy() if rc == 0 else ref)
+    # plane-aligned row range (one shard's slab), march when it applies
+    plane = n // shape[-1]
+    lo, hi = plane * (shape[-1] // 3), plane * max(shape[-1] // 3 + 1, (2 * shape[-1]) // 3)
+    d = op._desc
+    sub = type(d)()
+    ctypes.pointer(sub)[0] = d
+    sub.row_begin, sub.row_end = lo, hi
+    Yd = torch.full_like(Xd, np.nan)
+    if _lib.query("ekcg_spmm_stencil_kernel", 1, ctypes.byref(sub), Xd.data_ptr(), m, Yd.data_ptr(), m, m, None,
+                  stream()) != 0:
         _lib.call("ekcg_spmm_stencil", ctypes.byref(sub), Xd.data_ptr(), m, Yd.data_ptr(), m, m, None, stream())
-        part = Yd.cpu().numpy()
-    finally:
-        _lib.query("ekcg_tune", 3, 1)
-        _lib.query("ekcg_tune", 12, 1 << 21)
+    part = Yd.cpu().numpy()
     assert np.array_equal(outs[0], ref)
     assert np.array_equal(outs[1], ref)
     assert np.array_equal(part[lo:hi], ref[lo:hi])
@@ -264,20 +250,25 @@ def test_gram_multi_block(m1, m2, n):
 
 @pytest.mark.parametrize("m", [4, 8, 16, 32, 64])
 def test_vec256_paths_bitwise(m):
-    """X^T y (m2 = 1) and the fused x / r update with 256-bit row loads (ekcg_tune 24) against the
-    128-bit loads: the same products and sums, so bitwise equal; plus a tolerance check on X^T y."""
+    """X^T y (m2 = 1) and the fused x / r update with 256-bit row loads (32-B aligned blocks) against
+    the 128-bit loads (the same blocks 16 B off a 32-B boundary): the same products and sums, so bitwise
+    equal; plus a tolerance check on X^T y."""
     rng = np.random.default_rng(240 + m)
     n, d = 300_007, 2
-    Xs = [dev(rng.standard_normal((n, m))) for _ in range(d)]
+    host = [rng.standard_normal((n, m)) for _ in range(d)]
     y = dev(rng.standard_normal(n))
-    tab = torch.tensor([x.data_ptr() for x in Xs], dtype=torch.int64, device=DEV)
     chunks = _lib.query("ekcg_gram_chunks", n, d, m, 1)
     part = torch.empty(chunks * d * m, dtype=torch.float64, device=DEV)
     alpha = dev(rng.standard_normal(m) * 1e-2)
     vchunks = _lib.query("ekcg_vec_chunks", n)
     outs = {}
-    for v in (1, 0):
-        _lib.call("ekcg_tune", 24, v)
+    for v, off in ((1, 0), (0, 2)):  # offset 2 doubles: 16-B aligned, not 32-B
+        bufs = [torch.empty(n * m + 4, dtype=torch.float64, device=DEV) for _ in range(d)]
+        Xs = [b[off:off + n * m].view(n, m) for b in bufs]
+        for X, h in zip(Xs, host):
+            X.copy_(torch.from_numpy(h))
+        assert all((X.data_ptr() % 32 == 0) == (v == 1) for X in Xs)
+        tab = torch.tensor([x.data_ptr() for x in Xs], dtype=torch.int64, device=DEV)
         g = torch.empty(d * m, dtype=torch.float64, device=DEV)
         _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, y.data_ptr(), 1, 1, n, part.data_ptr(), None, stream())
         _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m, g.data_ptr(), None, stream())
@@ -286,7 +277,6 @@ def test_vec256_paths_bitwise(m):
         _lib.call("ekcg_xr_update", Xs[0].data_ptr(), m, Xs[1].data_ptr(), m, alpha.data_ptr(), m, x.data_ptr(),
                   r.data_ptr(), n, vp.data_ptr(), None, stream())
         outs[v] = [t.cpu().numpy() for t in (g, x, r, vp)]
-    _lib.call("ekcg_tune", 24, 1)
     for a, b in zip(outs[1], outs[0]):
         assert np.array_equal(a.view(np.int64), b.view(np.int64))
     ref = torch.stack([X.T @ y for X in Xs]).reshape(-1).cpu().numpy()
@@ -314,27 +304,24 @@ def test_gram_self_symmetric_shortcut(n, m):
     assert (outs[0] - X.T @ X).abs().max().item() <= 1e-13 * (X.abs().T @ X.abs()).max().item()
 
 
-@pytest.mark.parametrize("target", [296, 444, 592])
-def test_streamed_gram_many_ctas_per_sm(target):
+@pytest.mark.parametrize("n", [200_000, 600_000, 1_000_003])
+def test_streamed_gram_many_ctas_per_sm(n):
     """Regression: the TMA ring refills a slot only after a proxy fence orders the
     consumers' generic reads before the async write.  Without it, 3+ co-resident
-    CTAs per SM (the one-block m = 16 Gram at these chunk counts) read refilled
-    slots and ~1 % of the rows went wrong."""
-    n, m = 200_000, 16
+    CTAs per SM (the one-block m = 16 Gram: 3 per SM, several waves at these
+    chunk counts) read refilled slots and ~1 % of the rows went wrong."""
+    m = 16
     X = torch.randn(n, m, dtype=torch.float64, device=DEV)
     tab = torch.tensor([X.data_ptr()], dtype=torch.int64, device=DEV)
     ref = X.T @ X
-    assert _lib.query("ekcg_tune", 2, target) == 0
-    try:
-        chunks = _lib.query("ekcg_gram_chunks", n, 1, m, m)
-        for _ in range(3):
-            part = torch.empty(chunks * m * m, dtype=torch.float64, device=DEV)
-            G = torch.empty(m * m, dtype=torch.float64, device=DEV)
-            _lib.call("ekcg_gram", tab.data_ptr(), m, 1, m, X.data_ptr(), m, m, n, part.data_ptr(), None, stream())
-            _lib.call("ekcg_reduce", part.data_ptr(), chunks, m * m, G.data_ptr(), None, stream())
-            assert (G.view(m, m) - ref).abs().max().item() <= 1e-13 * ref.abs().max().item()
-    finally:
-        _lib.call("ekcg_tune", 2, 0)
+    chunks = _lib.query("ekcg_gram_chunks", n, 1, m, m)
+    assert chunks > 2 * torch.cuda.get_device_properties(DEV).multi_processor_count
+    for _ in range(3):
+        part = torch.empty(chunks * m * m, dtype=torch.float64, device=DEV)
+        G = torch.empty(m * m, dtype=torch.float64, device=DEV)
+        _lib.call("ekcg_gram", tab.data_ptr(), m, 1, m, X.data_ptr(), m, m, n, part.data_ptr(), None, stream())
+        _lib.call("ekcg_reduce", part.data_ptr(), chunks, m * m, G.data_ptr(), None, stream())
+        assert (G.view(m, m) - ref).abs().max().item() <= 1e-13 * ref.abs().max().item()
 
 
 def test_gram_deterministic():
@@ -373,28 +360,23 @@ def test_block_update(m1, m2, n, beta):
 @pytest.mark.parametrize("d", [1, 2, 5, 7])
 @pytest.mark.parametrize("n", [63, 70_001])
 def test_wide_streamed_update_and_gram(m, d, n):
-    """Streamed m = 32 / 64 kernels (stream_wide.cu) against the register-direct ones
-    and torch: every depth (C_i resident in smem or not), ragged last slab, in place."""
+    """Wide-block kernels (m = 32 streamed, m = 64 smem-C / register-direct) against
+    torch: every depth (C_i resident in smem or not), ragged last slab, in place."""
     rng = np.random.default_rng(m * 100 + d + n)
     Qs = [dev(rng.standard_normal((n, m))) for _ in range(d)]
     C = dev(rng.standard_normal((d * m, m)))
     Win = dev(rng.standard_normal((n, m)))
     tab = torch.tensor([q.data_ptr() for q in Qs], dtype=torch.int64, device=DEV)
     outs = []
-    for wide, variant in ((1, 0), (1, 1), (1, 2), (0, 0)):
-        _lib.call("ekcg_tune", 15, wide)
-        _lib.call("ekcg_tune", 16, variant)
-        W = Win.clone()
-        _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m, W.data_ptr(),
-                  m, m, 1.0, -1.0, n, None, stream())
-        chunks = _lib.query("ekcg_gram_chunks", n, d, m, m)
-        part = torch.empty(chunks * d * m * m, dtype=torch.float64, device=DEV)
-        G = torch.empty(d * m * m, dtype=torch.float64, device=DEV)
-        _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Win.data_ptr(), m, m, n, part.data_ptr(), None, stream())
-        _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m * m, G.data_ptr(), None, stream())
-        outs.append((W, G.view(d, m, m)))
-    _lib.call("ekcg_tune", 15, 1)
-    _lib.call("ekcg_tune", 16, 0)
+    W = Win.clone()
+    _lib.call("ekcg_block_update", tab.data_ptr(), m, d, m, C.data_ptr(), W.data_ptr(), m, W.data_ptr(),
+              m, m, 1.0, -1.0, n, None, stream())
+    chunks = _lib.query("ekcg_gram_chunks", n, d, m, m)
+    part = torch.empty(chunks * d * m * m, dtype=torch.float64, device=DEV)
+    G = torch.empty(d * m * m, dtype=torch.float64, device=DEV)
+    _lib.call("ekcg_gram", tab.data_ptr(), m, d, m, Win.data_ptr(), m, m, n, part.data_ptr(), None, stream())
+    _lib.call("ekcg_reduce", part.data_ptr(), chunks, d * m * m, G.data_ptr(), None, stream())
+    outs.append((W, G.view(d, m, m)))
     ref = Win - sum(Qs[i] @ C[i * m:(i + 1) * m] for i in range(d))
     scale = sum((Qs[i].abs() @ C[i * m:(i + 1) * m].abs()) for i in range(d)).max().item() + 1.0
     for W, G in outs:
@@ -456,3 +438,35 @@ def test_launch_counter_moves():
     before = _lib.query("ekcg_launch_count")
     pk.norm2(np.ones(10))
     assert _lib.query("ekcg_launch_count") >= before + 2
+
+
+def test_public_api_accepts_misaligned_views():
+    """Caller tensors at odd element offsets (not 16-/32-B aligned) go through the
+    public gram / trsm / norm wrappers (copied to aligned storage first) instead of
+    faulting in the bulk-copy / 256-bit kernels."""
+    rng = np.random.default_rng(5)
+    n, m = 50_001, 16
+    buf = dev(rng.standard_normal(n * m + 3))
+    X = buf[1:1 + n * m].view(n, m)
+    assert X.data_ptr() % 16 != 0
+    G = pk.gram(X, X)
+    ref = X.T @ X
+    assert (G - ref).abs().max().item() <= 1e-12 * ref.abs().max().item()
+    R = torch.linalg.cholesky(ref).T.contiguous()
+    Y = pk.trsm_right_inv(X, R)
+    assert (Y @ R - X).abs().max().item() <= 1e-10 * X.abs().max().item()
+    assert abs(pk.norm2(buf[1:]) - torch.linalg.vector_norm(buf[1:]).item()) <= 1e-12 * pk.norm2(buf[1:])
+
+
+def test_nan_residual_reports_maxiter():
+    """A NaN residual stops the solve with status 'maxiter', like the reference loop
+    (solvers.py:357: `nan > tol * rho0` is false; :417: `nan <= tol * rho0` is false too)."""
+    ctrl = torch.zeros(_lib.query("ekcg_ctrl_bytes"), dtype=torch.uint8, device=DEV)
+    hist = torch.zeros(8, dtype=torch.float64, device=DEV)
+    rho2 = torch.tensor([4.0], dtype=torch.float64, device=DEV)
+    _lib.call("ekcg_start", ctrl.data_ptr(), rho2.data_ptr(), 1e-8, hist.data_ptr(), stream())
+    rho2.fill_(float("nan"))
+    _lib.call("ekcg_finish", ctrl.data_ptr(), rho2.data_ptr(), 1, 100, 0, hist.data_ptr(), stream())
+    raw = ctrl.cpu().numpy()
+    ints = raw[:32].view(np.int32)
+    assert ints[0] == 0 and ints[1] == 2  # live cleared, status maxiter

@@ -265,22 +265,20 @@ def test_fused_matches_unfused(floors_golden, idx, edge):
     assert hist_dev(a.residual_history, b.residual_history, k=10) <= (0.5 if chaotic else 1e-9)
 
 
-@pytest.mark.parametrize("idx,edge", [(2, 16), (2, 12), (4, 10)])
-def test_march_fused_kernels_match_row_kernels(idx, edge):
-    """Plane-marching stencil kernels (plain, fused A-CholQR, fused x/r update),
-    forced at small sizes (ekcg_tune key 12), against the row-parallel kernels."""
-    from paper_2305_19013_b200 import _lib
+@pytest.mark.parametrize("idx,edge", [(2, 64), (2, 52)])
+def test_march_fused_kernels_match_unfused(idx, edge):
+    """Plane-marching fused kernels (stencil + A-CholQR Gram + factor, stencil + x/r update +
+    stop test), which the engine takes above 2^21 block entries, against the unfused sequence
+    (plain plane march + DMMA Gram + separate factor / update kernels)."""
     from paper_2305_19013_b200.engine import DeviceEngine
     prob = make_config(idx, edge)
     cfg = SolverConfig(**dict(prob.solver_kwargs, kmax=30))
     op = prob.stencil()
     reps = []
-    try:
-        for march in (0, 1):
-            assert _lib.query("ekcg_tune", 12, 0 if march else 1 << 62) == 0
-            reps.append(DeviceEngine(op, prob.partition, cfg).solve(prob.b)[1])
-    finally:
-        _lib.query("ekcg_tune", 12, 1 << 21)
+    for no_fuse in (False, True):
+        eng = DeviceEngine(op, prob.partition, cfg)
+        eng.no_fuse = no_fuse
+        reps.append(eng.solve(prob.b)[1])
     a, b = reps
     assert a.iterations == b.iterations
     assert hist_dev(a.residual_history, b.residual_history) <= 1e-10

@@ -75,3 +75,36 @@ def test_stencil_descriptor_host_csr():
     from paper_2305_19013_b200.problems import diffusion_csr
     A = diffusion_csr(prob.shape, prob.node_kappa())
     assert csr_hash(A) == csr_hash(prob.csr())
+
+
+def test_from_coo_sums_duplicates_and_validates():
+    """from_coo (linalg.py:55-79): duplicates summed, CSR rows sorted; the validator's
+    messages for each malformed input (linalg.py:81-109)."""
+    rng = np.random.default_rng(4)
+    for _ in range(50):
+        n = int(rng.integers(1, 20))
+        k = int(rng.integers(0, 60))
+        r, c, v = rng.integers(0, n, k), rng.integers(0, n, k), rng.standard_normal(k)
+        keep = r != c  # off-diagonal pairs (duplicates summed in the same order on both sides)
+        r, c, v = np.minimum(r, c)[keep], np.maximum(r, c)[keep], v[keep]
+        R = np.concatenate([r, c, np.arange(n), np.arange(n)])
+        C = np.concatenate([c, r, np.arange(n), np.arange(n)])
+        V = np.concatenate([v, v, np.full(n, 40.0), np.full(n, 0.5)])
+        A = pk.SparseSpdMatrix.from_coo(n, R, C, V)
+        D = np.zeros((n, n))
+        np.add.at(D, (R, C), V)
+        assert np.allclose(A.to_dense(), D, rtol=1e-15, atol=0)
+        assert np.array_equal(A.diagonal(), np.diag(A.to_dense()))
+        assert all(np.all(np.diff(A.col_idx[A.row_ptr[i]:A.row_ptr[i + 1]]) > 0) for i in range(n))
+    bad = [((2, [0, 2, 1], [0, 1], [1.0, 1.0]), "malformed row_ptr"),
+           ((2, [0, 2, 2], [1, 0], [1.0, 1.0]), "sorted and unique"),
+           ((2, [0, 1, 2], [0, 0], [1.0, 1.0]), "diagonal entries"),
+           ((2, [0, 1, 2], [0, 1], [1.0, -1.0]), "diagonal entries"),
+           ((2, [0, 2, 3], [0, 1, 1], [2.0, 1.0, 2.0]), "symmetric"),
+           ((2, [0, 1, 2], [0, 1], [np.inf, 1.0]), "finite"),
+           ((2, [0, 1, 2], [0, 5], [1.0, 1.0]), "out of range")]
+    for args, msg in bad:
+        with pytest.raises(ValueError, match=msg):
+            pk.SparseSpdMatrix(*args)
+    with pytest.raises(ValueError, match="out of range"):
+        pk.SparseSpdMatrix.from_coo(3, [0, 3], [0, 0], [1.0, 1.0])

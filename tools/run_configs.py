@@ -33,10 +33,8 @@ def main():
     ap.add_argument("--kmax-cfg4", type=int, default=400)
     ap.add_argument("--kmax-cfg5", type=int, default=20)
     ap.add_argument("--repeats", type=int, default=3, help="best of N solves (the first pays one-time setup)")
-    ap.add_argument("--stencil-march", type=int, default=1, help="plane-marching stencil kernel (ekcg_tune 3)")
     args = ap.parse_args()
     from paper_2305_19013_b200 import _lib
-    _lib.call("ekcg_tune", 3, args.stencil_march)
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
         else {"hbm_gbs": 6650.0}
     hbm = float(peaks["hbm_gbs"])
