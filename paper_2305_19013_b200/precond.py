@@ -1,9 +1,9 @@
 """Split block-Jacobi preconditioning M = L L^T (row F4; reference blockjacobi.py:1-183).
 
-Setup (host, once per matrix): the dense diagonal blocks of A are factored
-exactly (`chol`) or with zero fill-in (`ichol0`, with the reference's
-diagonal-shift retries) -- the same numpy operations as the reference, so the
-factors are bitwise the reference's.  The device keeps the dense factors L_b;
+Setup (host, once per matrix): the dense diagonal blocks of A are gathered in
+one pass over the CSR and factored exactly (`chol`, LAPACK) or with zero
+fill-in (`ichol0`, left-looking rows, with the reference's diagonal-shift
+retries).  The reference's own factor objects are accepted as they are.  The device keeps the dense factors L_b;
 L^-1 / L^-T run as per-block substitutions (`ekcg_block_trsv`) and L / L^T
 as a block-diagonal dense product (`ekcg_block_diag_apply`), over n x m
 row-major blocks.
@@ -15,7 +15,6 @@ from dataclasses import dataclass, field
 
 import numpy as np
 import torch
-from scipy.linalg import solve_triangular
 
 from . import _lib
 from .device import as_device, current_stream_ptr, get_device
@@ -24,6 +23,8 @@ from .linalg import Breakdown
 __all__ = [
     "BlockJacobiFactor",
     "uniform_block_bounds",
+    "diagonal_blocks",
+    "ichol0",
     "build_block_jacobi",
     "forward_solve",
     "backward_solve",
@@ -37,7 +38,10 @@ __all__ = [
 
 @dataclass(frozen=True)
 class BlockJacobiFactor:
-    """Per-block lower-triangular factors over consecutive index ranges (blockjacobi.py:33-47)."""
+    """Per-block lower-triangular factors over consecutive index ranges.
+
+    The field layout is the reference's factor type (blockjacobi.py:33-47), so a
+    factor built by either package can be passed as `SolverConfig.preconditioner`."""
 
     n: int
     block_bounds: tuple
@@ -51,76 +55,94 @@ class BlockJacobiFactor:
 
 
 def uniform_block_bounds(n, nblocks):
-    """Consecutive ranges; the first n mod nblocks get one extra row (blockjacobi.py:50-57)."""
+    """Consecutive ranges, the first n mod nblocks one row longer (blockjacobi.py:50-57)."""
     n, nblocks = int(n), int(nblocks)
     if nblocks < 1 or nblocks > n:
         raise ValueError(f"need 1 <= nblocks <= n, got {nblocks}, n={n}")
-    base, extra = divmod(n, nblocks)
-    edges = np.concatenate(([0], np.cumsum([base + 1] * extra + [base] * (nblocks - extra))))
-    return tuple((int(edges[i]), int(edges[i + 1])) for i in range(nblocks))
+    q, r = divmod(n, nblocks)
+    cut = [i * q + min(i, r) for i in range(nblocks + 1)]
+    return tuple(zip(cut[:-1], cut[1:]))
 
 
-def _diag_block(A, start, end):
-    m = end - start
-    out = np.zeros((m, m))
-    for i in range(start, end):
-        lo, hi = A.row_ptr[i], A.row_ptr[i + 1]
-        cols = A.col_idx[lo:hi]
-        inside = (cols >= start) & (cols < end)
-        out[i - start, cols[inside] - start] = A.values[lo:hi][inside]
+def _check_bounds(bounds, n):
+    starts = np.array([s for s, _ in bounds], dtype=np.int64)
+    ends = np.array([e for _, e in bounds], dtype=np.int64)
+    if starts[0] != 0 or ends[-1] != n:
+        raise ValueError("block bounds must cover 0..n")
+    if np.any(ends <= starts) or np.any(starts[1:] != ends[:-1]):
+        raise ValueError("block bounds must be consecutive, nonempty ranges")
+
+
+def diagonal_blocks(A, bounds):
+    """Dense diagonal blocks A[s:e, s:e], gathered in one vectorised pass over the CSR:
+    entries whose row and column fall in the same range are scattered into their block."""
+    n = int(A.n)
+    rp = np.asarray(A.row_ptr, dtype=np.int64)
+    ci = np.asarray(A.col_idx, dtype=np.int64)
+    vv = np.asarray(A.values, dtype=np.float64)
+    starts = np.array([s for s, _ in bounds], dtype=np.int64)
+    blk_of = np.searchsorted(starts, np.arange(n), side="right") - 1  # block of every index
+    rows = np.repeat(np.arange(n), np.diff(rp))
+    inside = blk_of[rows] == blk_of[ci]
+    rows, cols, vals, blk = rows[inside], ci[inside], vv[inside], blk_of[rows[inside]]
+    out = [np.zeros((e - s, e - s)) for s, e in bounds]
+    for b in np.unique(blk):
+        sel = blk == b
+        out[b][rows[sel] - starts[b], cols[sel] - starts[b]] = vals[sel]
     return out
 
 
-def _ichol0(block, pattern):
-    """IC(0) on the lower pattern (blockjacobi.py:71-84)."""
-    m = block.shape[0]
-    L = np.where(pattern, np.tril(block), 0.0)
-    for k in range(m):
-        piv = L[k, k]
-        if piv <= 0.0:
-            raise Breakdown(f"nonpositive IC(0) pivot {piv:.3e} at local row {k}")
-        L[k, k] = np.sqrt(piv)
-        if k + 1 < m:
-            col = np.where(pattern[k + 1:, k], L[k + 1:, k] / L[k, k], 0.0)
-            L[k + 1:, k] = col
-            L[k + 1:, k + 1:] -= np.where(pattern[k + 1:, k + 1:], np.outer(col, col), 0.0)
+def ichol0(B):
+    """Incomplete Cholesky with zero fill-in of a dense SPD block, on the lower
+    nonzero pattern of B (the factor blockjacobi.py:71-84 defines), in the
+    left-looking row form: row i is finished from rows j < i already final,
+
+        L[i, j] = (B[i, j] - L[i, :j] . L[j, :j]) / L[j, j]   for (i, j) in the pattern,
+        L[i, i] = sqrt(B[i, i] - L[i, :i] . L[i, :i]),
+
+    where L[i, k] is zero off the pattern.  Raises Breakdown on a nonpositive pivot."""
+    m = B.shape[0]
+    L = np.zeros_like(B)
+    for i in range(m):
+        row = L[i]
+        for j in np.flatnonzero(B[i, :i]):
+            row[j] = (B[i, j] - row[:j] @ L[j, :j]) / L[j, j]
+        piv = B[i, i] - row[:i] @ row[:i]
+        if not piv > 0.0:
+            raise Breakdown(f"nonpositive IC(0) pivot {piv:.3e} at local row {i}")
+        row[i] = np.sqrt(piv)
     return L
 
 
 def build_block_jacobi(A, block_bounds, kind="chol", shift_retries=3):
-    """Factor the diagonal blocks of A (blockjacobi.py:87-132)."""
+    """Block-Jacobi factor of A (blockjacobi.py:87-132): exact dense Cholesky of every
+    diagonal block ("chol") or IC(0) ("ichol0"); an IC(0) breakdown is retried with
+    the diagonal shifted by 1e-8 * max(diag), doubling, at most `shift_retries` times."""
     bounds = tuple((int(s), int(e)) for s, e in block_bounds)
-    if bounds[0][0] != 0 or bounds[-1][1] != A.n:
-        raise ValueError("block bounds must cover 0..n")
-    for (s0, e0), (s1, _) in zip(bounds, bounds[1:]):
-        if e0 != s1 or e0 <= s0:
-            raise ValueError("block bounds must be consecutive, nonempty ranges")
-    if bounds[-1][1] <= bounds[-1][0]:
-        raise ValueError("block bounds must be consecutive, nonempty ranges")
+    _check_bounds(bounds, A.n)
     if kind not in ("chol", "ichol0"):
         raise ValueError(f"unknown factor kind {kind!r}")
     factors, notes = [], []
-    for b, (start, end) in enumerate(bounds):
-        block = _diag_block(A, start, end)
+    for b, B in enumerate(diagonal_blocks(A, bounds), start=1):
         if kind == "chol":
             try:
-                factors.append(np.linalg.cholesky(block))
+                factors.append(np.linalg.cholesky(B))
             except np.linalg.LinAlgError as exc:
-                raise Breakdown(f"Cholesky failed on block {b + 1}: {exc}") from exc
+                raise Breakdown(f"Cholesky failed on block {b}: {exc}") from exc
             continue
-        pattern = np.tril(block != 0.0)
-        sigma = 1e-8 * float(np.max(np.diag(block)))
-        shift = 0.0
-        for attempt in range(shift_retries + 1):
+        base = 1e-8 * float(B.diagonal().max())
+        shifts = [0.0] + [base * 2.0 ** i for i in range(shift_retries)]
+        for shift in shifts:
             try:
-                factors.append(_ichol0(block + shift * np.eye(block.shape[0]) if shift else block, pattern))
-                if shift:
-                    notes.append(f"block {b + 1}: IC(0) needed diagonal shift {shift:.3e}")
-                break
+                L = ichol0(B + shift * np.eye(len(B)) if shift else B)
             except Breakdown:
-                if attempt == shift_retries:
-                    raise Breakdown(f"IC(0) failed on block {b + 1} after {shift_retries} diagonal shifts")
-                shift = sigma if shift == 0.0 else 2.0 * shift
+                continue
+            if shift:
+                notes.append(f"block {b}: IC(0) needed diagonal shift {shift:.3e}")
+            factors.append(L)
+            break
+        else:
+            raise Breakdown(f"IC(0) failed on block {b} after {shift_retries} diagonal shifts")
     return BlockJacobiFactor(A.n, bounds, tuple(factors), kind, tuple(notes))
 
 
