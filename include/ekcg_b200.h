@@ -60,7 +60,17 @@ typedef struct EkcgStencil {
     const double* hx;
     const double* hy;
     const double* hz;
+    /* optional, tile fields only: per-node coefficient rows built once per operator by
+     * ekcg_stencil_coefs with the kernels' own arithmetic (bitwise the values computed on
+     * the fly).  Row i holds EKCG_COEF_STRIDE(dim) doubles in slot order (2-D: y-, x-,
+     * diag, x+, y+, pad; 3-D: z-, y-, x-, diag, x+, y+, z+, pad); absent neighbours hold
+     * +0.0 (presence still follows from the grid position).  Rows are addressed by global
+     * row index.  Costs 48 (2-D) / 64 (3-D) bytes per node and application, in exchange
+     * for the tile lookups and face bookkeeping of every node in every column chunk. */
+    const double* coef;
 } EkcgStencil;
+
+#define EKCG_COEF_STRIDE(dim) ((dim) == 3 ? 8 : 6)
 
 /* ---- sparse operator and T^t split ------------------------------------ */
 
@@ -99,6 +109,11 @@ int ekcg_spmm_csr_kernel(int form, const long long* row_ptr, const int* col_idx,
  * CSR that generators.py:25-60 assembles for the same kappa. */
 int ekcg_spmm_stencil(const EkcgStencil* desc, const double* X, int ldx, double* Y, int ldy,
                       int m, const int* live, void* stream);
+
+/* Fill coef (n x EKCG_COEF_STRIDE(dim) doubles, n = nx*ny*nz, all rows regardless of
+ * row_begin / row_end) with the per-node coefficient rows of a kfield descriptor (its own
+ * coef pointer is ignored).  Attach the array to the descriptor's `coef` afterwards. */
+int ekcg_stencil_coefs(const EkcgStencil* desc, double* coef, void* stream);
 
 /* ekcg_spmm_stencil with an explicit kernel form: 0 = automatic, 1 = the TMA
  * plane march at any size (-1 when it does not apply: m % 4, alignment, or a

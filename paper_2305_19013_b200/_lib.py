@@ -25,6 +25,7 @@ SIGNATURES = {
     "ekcg_spmm_stencil": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p, c_void_p]),
     "ekcg_spmm_csr_kernel": (c_int, [c_int, c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_void_p, c_int,
                                      c_longlong, c_int, c_void_p, c_void_p]),
+    "ekcg_stencil_coefs": (c_int, [c_void_p, c_void_p, c_void_p]),
     "ekcg_spmm_stencil_kernel": (c_int, [c_int, c_void_p, c_void_p, c_int, c_void_p, c_int, c_int, c_void_p,
                                          c_void_p]),
     "ekcg_gram_chunks": (c_int, [c_longlong, c_int, c_int, c_int]),
@@ -78,6 +79,7 @@ class EkcgStencil(ctypes.Structure):
         ("row_begin", c_longlong), ("row_end", c_longlong),
         ("kself", c_void_p),
         ("hx", c_void_p), ("hy", c_void_p), ("hz", c_void_p),
+        ("coef", c_void_p),
     ]
 
 

@@ -505,6 +505,44 @@ extern "C" int ekcg_spmm_csr_kernel(int form, const long long* row_ptr, const in
     return spmm_csr_impl(form, row_ptr, col_idx, values, X, ldx, Y, ldy, n, m, live, as_stream(stream));
 }
 
+// Per-node coefficient rows of a kfield operator (ekcg_stencil_coefs): the same stencil_coef arithmetic the
+// kernels run on the fly (descriptor without a table), stored once.
+__global__ void __launch_bounds__(256)
+stencil_coef_build_kernel(EkcgStencil s, UniformFaces uf, double* __restrict__ coef, long long n) {
+    const int S = (s.dim == 3) ? 8 : 6;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        const unsigned x = (unsigned)(i % s.nx);
+        const long long rest = i / s.nx;
+        const unsigned y = (unsigned)(rest % s.ny), z = (unsigned)(rest / s.ny);
+        double v[7];
+        if (s.dim == 3) stencil_coef(s, uf, x, y, z, v);
+        else stencil_coef(s, uf, x, (unsigned)rest, 0u, v);
+        double* r = coef + S * i;
+        if (s.dim == 3) {
+            for (int q = 0; q < 7; ++q) r[q] = v[q];
+            r[7] = 0.0;
+        } else {
+            for (int q = 0; q < 5; ++q) r[q] = v[q + 1];
+            r[5] = 0.0;
+        }
+    }
+}
+
+extern "C" int ekcg_stencil_coefs(const EkcgStencil* desc, double* coef, void* stream) {
+    EkcgStencil s;
+    UniformFaces uf;
+    long long n;
+    int rc = prepare_stencil(desc, s, uf, n);
+    if (rc != EKCG_OK) return rc;
+    if (s.kfield == nullptr || coef == nullptr || (reinterpret_cast<uintptr_t>(coef) & 15)) return EKCG_EINVAL;
+    s.coef = nullptr;  // compute every row on the fly
+    const long long blocks = (n + 255) / 256;
+    const unsigned grid = (unsigned)(blocks < (long long)device_sms() * 16 ? blocks : (long long)device_sms() * 16);
+    launch_k(stencil_coef_build_kernel, grid, 256, 0, as_stream(stream), s, uf, coef, n);
+    ++g_ekcg_launches;
+    return launch_status();
+}
+
 // Stencil kernel forms (ekcg_spmm_stencil_kernel): 0 automatic (the TMA plane march above
 // kMarchMinWork block entries, else the row-parallel kernel), 1 the plane march at any size, 2 the
 // row-parallel kernel.  Both kernels reproduce the generator's CSR association, so they agree bit for bit.

@@ -52,10 +52,39 @@ __device__ __forceinline__ double face_hi(const EkcgStencil& s, double c, const 
 
 // Coefficients of the node (x, y, z): v[0..6] = z-, y-, x-, diag, x+, y+, z+
 // (absent neighbours: 0) and the presence mask (bit q = slot q present).
+// Per-node coefficient row (2-D: slots 1..5, 3-D: slots 0..6) from the table built by ekcg_stencil_coefs.
+__device__ __forceinline__ void coef_row(const EkcgStencil& s, long long i, double (&v)[7]) {
+    if (s.dim == 3) {
+        const double2* r = reinterpret_cast<const double2*>(s.coef + 8 * i);
+        const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3);
+        v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y; v[4] = c.x; v[5] = c.y; v[6] = d.x;
+    } else {
+        const double2* r = reinterpret_cast<const double2*>(s.coef + 6 * i);
+        const double2 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
+        v[0] = 0.0; v[1] = a.x; v[2] = a.y; v[3] = b.x; v[4] = b.y; v[5] = c.x; v[6] = 0.0;
+    }
+}
+
+__device__ __forceinline__ unsigned stencil_mask(const EkcgStencil& s, unsigned x, unsigned y, unsigned z) {
+    const bool three = (s.dim == 3);
+    unsigned mk = 1u << 3;
+    if (three && z > 0)          mk |= 1u << 0;
+    if (y > 0)                   mk |= 1u << 1;
+    if (x > 0)                   mk |= 1u << 2;
+    if (x < s.nx - 1)            mk |= 1u << 4;
+    if (y < s.ny - 1)            mk |= 1u << 5;
+    if (three && z < s.nz - 1)   mk |= 1u << 6;
+    return mk;
+}
+
 __device__ __forceinline__ unsigned stencil_coef(const EkcgStencil& s, const UniformFaces& uf, unsigned x,
                                                  unsigned y, unsigned z, double (&v)[7]) {
     const unsigned nx = s.nx, ny = s.ny, nz = s.nz;
     const bool three = (s.dim == 3);
+    if (s.coef != nullptr) {
+        coef_row(s, three ? ((long long)z * ny + y) * nx + x : (long long)y * nx + x, v);
+        return stencil_mask(s, x, y, z);
+    }
     double fzl = 0.0, fzh = 0.0, fyl = 0.0, fyh = 0.0, fxl = 0.0, fxh = 0.0;
     double diag = 0.0;
     if (s.kfield == nullptr) {
@@ -121,7 +150,11 @@ __device__ __forceinline__ int stencil_row(const EkcgStencil& s, const UniformFa
 
     double fzl = 0.0, fzh = 0.0, fyl = 0.0, fyh = 0.0, fxl = 0.0, fxh = 0.0;
     double diag = 0.0;
-    if (s.kfield == nullptr) {
+    if (s.coef != nullptr) {
+        double v[7];
+        coef_row(s, i, v);
+        fzl = -v[0]; fyl = -v[1]; fxl = -v[2]; diag = v[3]; fxh = -v[4]; fyh = -v[5]; fzh = -v[6];
+    } else if (s.kfield == nullptr) {
         if (three) {
             if (z < nz - 1) { fzh = uf.fz; diag = add_rn(diag, fzh); }
             if (z > 0)      { fzl = uf.fz; diag = add_rn(diag, fzl); }
@@ -240,6 +273,8 @@ static inline int prepare_stencil(const EkcgStencil* desc, EkcgStencil& s, Unifo
         s.row_end = n;
     }
     if (s.row_begin < 0 || s.row_begin >= s.row_end || s.row_end > n) return EKCG_EINVAL;
+    // the per-node table only stands in for a kfield operator's coefficients (16-B aligned rows)
+    if (s.kfield == nullptr || (reinterpret_cast<uintptr_t>(s.coef) & 15)) s.coef = nullptr;
     uf = UniformFaces{};
     if (s.kfield == nullptr) {
         uf.fz = host_face(s.cz, s.kconst);

@@ -104,6 +104,10 @@ class DeviceEngine:
         # fused stages in use when the operator/width allow: "prechol" (update2 + Graw + S0),
         # "cholinv" (A W0 + G + S), "vec" (W0 S + alpha), "xr" (A W_k + x/r + finish)
         self.fuse = {"cholinv", "vec", "xr"}
+        # small (launch-latency-bound) blocks also fuse the second CGS2 update with Graw and the
+        # Pre-CholQR factor: config 1 10.2k -> 11.9k it/s; on config 2 (4.2 M block entries) the
+        # fused kernel is slower (tools/ab_graphs.py --prechol)
+        self.fuse_prechol_max = 1 << 20
         # cache A Q next to every retained Q (reference scheme, aortho.py:82-87) or
         # recompute the projections as Q^T (A W) with A symmetric ("lean": w + 2
         # blocks of HBM instead of 2w + 3; two extra operator applications per
@@ -435,7 +439,7 @@ class DeviceEngine:
                 for s0, e, wg in groups:  # all coefficients from the same W (classical GS)
                     self._gram(aq_addr(s0), wg, e - s0, wg, W, m, m, C.data_ptr() + F64 * off, tag="hist_gram")
                     off += (e - s0) * wg * m
-                if fused and pas == 1 and "prechol" in self.fuse:
+                if fused and pas == 1 and ("prechol" in self.fuse or n * m <= self.fuse_prechol_max):
                     # W'' = W' - Q C2 fused with Graw = W''^T W'' and the Pre-CholQR factor
                     self._timed("hist_update", lambda: _lib.call(
                         "ekcg_update_prechol", q_addr(0), m, d, C.data_ptr(), WA, m, WA, m, m, n,

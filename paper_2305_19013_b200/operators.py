@@ -136,10 +136,24 @@ class StencilOperator:
             desc.kconst = 0.0
         self.tile = (desc.tx, desc.ty, desc.tz)
         self._desc = desc
+        self.coef = None
+        if self.field is not None and self.dim == 3:
+            # per-node coefficient rows, built once on the device by the kernels' own arithmetic
+            # (ekcg_stencil_coefs): every later application loads a row instead of recomputing the
+            # tile lookups and faces of each node in each column chunk.  Measured: config-3 march
+            # 0.363 -> 0.326 ms; in 2-D (config 5) the extra 48 B per node made it 1.7 % slower
+            # (tools/probe_stencil.py), so 2-D fields keep the on-the-fly coefficients.
+            stride = 8 if self.dim == 3 else 6
+            self.coef = torch.empty(self.n * stride, dtype=torch.float64, device=self.device)
+            _lib.call("ekcg_stencil_coefs", ctypes.byref(desc), self.coef.data_ptr(),
+                      current_stream_ptr(self.device))
+            desc.coef = self.coef.data_ptr()
 
     def matrix_bytes(self):
-        """Bytes of operator data streamed per application (the kappa tile field)."""
-        return 0 if self.field is None else 8 * self.field.numel()
+        """M_A of the SURVEY 8(d) traffic model: 0 for constant kappa, 8 n (a node-kappa array) for a
+        kappa field.  The kernels actually stream the per-node coefficient table (48 n / 64 n bytes
+        in 2-D / 3-D); DESIGN.md section 3 and the ncu traffic columns account for it."""
+        return 0 if self.field is None else 8 * self.n
 
     def node_kappa(self):
         """Full node-kappa array (host), x fastest."""

@@ -130,3 +130,39 @@ def test_torch_in_torch_out(rng):
     out = pk.pre_cholqr(A, W)
     assert isinstance(out, torch.Tensor) and out.is_cuda
     assert a_err(out.cpu().numpy(), D) <= 1e-10
+
+
+@pytest.mark.parametrize("cond", [1e2, 1e4, 1e6])
+@pytest.mark.parametrize("m", [16, 64])
+def test_pre_cholqr_ill_conditioned_matches_substitution(rng, cond, m):
+    """The device applies R^-1 as an explicit upper inverse (DMMA block product) where the
+    reference substitutes (solve_triangular, linalg.py:187-196).  Across Pre-CholQR's operating
+    range (kappa(W) up to ~1e7: the Cholesky of W^T W sees kappa^2; beyond it both break down,
+    test_pre_cholqr_breakdown_matches_reference) the device result is as A-orthonormal as the
+    reference algorithm's (the oracle) and spans the same space."""
+    n = 3000
+    A, D = spd_csr(n, rng, 1.0, 100.0)
+    U, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    V, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    W = (U * np.geomspace(1.0, 1.0 / cond, m)) @ V.T
+    ours = pk.pre_cholqr(A, W)
+    ref, _ = orc.pre_cholqr_block(W.copy(), lambda X: D @ X)
+    e_ours, e_ref = a_err(ours, D), a_err(ref, D)
+    assert e_ours <= 10.0 * e_ref + 1e-12, (e_ours, e_ref)
+    # same column space: the projection of ours onto the reference basis loses nothing
+    G = ref.T @ D @ ours
+    assert np.linalg.norm(ref @ G - ours) <= 1e-6 * np.linalg.norm(ours), np.linalg.norm(ref @ G - ours)
+
+
+@pytest.mark.parametrize("m", [16, 64])
+def test_pre_cholqr_breakdown_matches_reference(rng, m):
+    """kappa(W) = 1e10: the Gram W^T W is singular to working precision; the device and the
+    reference algorithm both raise Breakdown (linalg.py:178-183) rather than return a basis."""
+    n = 3000
+    A, D = spd_csr(n, rng, 1.0, 100.0)
+    U, _ = np.linalg.qr(rng.standard_normal((n, m)))
+    W = U * np.geomspace(1.0, 1e-10, m)
+    with pytest.raises(pk.Breakdown):
+        pk.pre_cholqr(A, W)
+    with pytest.raises(orc.OracleBreakdown):
+        orc.pre_cholqr_block(W.copy(), lambda X: D @ X)

@@ -1,7 +1,6 @@
-# full verification of HEAD: gpu tests, smoke, default bench, reference arm, launch list
-mkdir -p gpurun_out
-timeout 1800 python -m pytest tests -q -m gpu -x 2>&1 | tail -6 > gpurun_out/tests.log; cat gpurun_out/tests.log
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; tail -3 gpurun_out/bench.err; cut -c1-600 gpurun_out/bench.json
-timeout 600 python bench.py --impl reference --steps 1 --warmup 0 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; cut -c1-400 gpurun_out/bench_ref.json
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_cur.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/ncu_l.log 2>&1; tail -1 gpurun_out/ncu_l.log
+# full GPU suite, smoke, default bench and reference arm (what the driver runs at round end)
+timeout 2400 python -m pytest tests/ -q -m gpu -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo "pytest rc $?"
+tail -15 gpurun_out/gpu_tests.log
+timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc $?"; tail -2 gpurun_out/smoke.log
+timeout 1200 python bench.py --steps 5 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc $?"; tail -2 gpurun_out/bench.err
+timeout 900 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err; echo "ref rc $?"
