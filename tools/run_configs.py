@@ -38,7 +38,7 @@ def main():
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() \
         else {"hbm_gbs": 6650.0}
     hbm = float(peaks["hbm_gbs"])
-    fp64 = 37.1e12  # measured DMMA peak (profiles/r01_fp64_peak.txt)
+    fp64 = json.loads((ROOT / "profiles" / "fp64_peak.json").read_text())["dmma_tflops"] * 1e12
     for idx in [int(c) for c in args.configs.split(",")]:
         t0 = time.perf_counter()
         prob = make_config(idx)
