@@ -155,7 +155,7 @@ int launch_gram16_stream(const double* const* Xs, int d, const double* Y, long l
 }
 
 // ---------------------------------------------------------------------------
-template <int R, int NS>
+template <int R, int NS, bool INIT>
 __global__ void __launch_bounds__(160)
 update16_stream_kernel(const double* const* __restrict__ Qs, int d, const double* __restrict__ C, const double* Win,
                        double* Wout, double beta, double sign, long long n, const int* __restrict__ live) {
@@ -203,11 +203,24 @@ update16_stream_kernel(const double* const* __restrict__ Qs, int d, const double
     for (long long sl = blockIdx.x; sl < slabs; sl += gridDim.x) {
         const long long rb = sl * R;
         const int rr = (int)min((long long)R, n - rb);
+        // the accumulators start from beta * Win (loads issued before the first ring wait) and the B
+        // fragments carry the sign (exact for +-1), so the tile is stored straight from them
         double acc[MR][2][2];
 #pragma unroll
-        for (int mr = 0; mr < MR; ++mr)
+        for (int mr = 0; mr < MR; ++mr) {
+            const long long r = rb + warp * 8 * MR + 8 * mr + lc;
 #pragma unroll
-            for (int nt = 0; nt < 2; ++nt) acc[mr][nt][0] = acc[mr][nt][1] = 0.0;
+            for (int nt = 0; nt < 2; ++nt) {
+                double2 w = make_double2(0.0, 0.0);
+                if (INIT && beta != 0.0 && r < n) {
+                    w = *reinterpret_cast<const double2*>(Win + r * M + 8 * nt + 2 * lr);
+                    w.x = beta * w.x;
+                    w.y = beta * w.y;
+                }
+                acc[mr][nt][0] = w.x;
+                acc[mr][nt][1] = w.y;
+            }
+        }
         for (int i = 0; i < d; ++i, ++t) {
             const int slot = (int)(t % NS);
             mbar_wait(&full[slot], (unsigned)((t / NS) & 1));
@@ -217,7 +230,8 @@ update16_stream_kernel(const double* const* __restrict__ Qs, int d, const double
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-                for (int nt = 0; nt < 2; ++nt) bfr[kk][nt] = Ci[(4 * kk + lr) * M + 8 * nt + lc];
+                for (int nt = 0; nt < 2; ++nt) bfr[kk][nt] = INIT ? sign * Ci[(4 * kk + lr) * M + 8 * nt + lc]
+                                                                  : Ci[(4 * kk + lr) * M + 8 * nt + lc];
 #pragma unroll
             for (int mr = 0; mr < MR; ++mr) {
                 const int row = warp * 8 * MR + 8 * mr + lc;
@@ -245,11 +259,14 @@ update16_stream_kernel(const double* const* __restrict__ Qs, int d, const double
 #pragma unroll
             for (int nt = 0; nt < 2; ++nt) {
                 const int b = 8 * nt + 2 * lr;
-                double2 o = make_double2(sign * acc[mr][nt][0], sign * acc[mr][nt][1]);
-                if (beta != 0.0) {
-                    const double2 wi = *reinterpret_cast<const double2*>(Win + r * M + b);
-                    o.x = beta * wi.x + o.x;
-                    o.y = beta * wi.y + o.y;
+                double2 o = make_double2(acc[mr][nt][0], acc[mr][nt][1]);
+                if (!INIT) {  // long sums: sign * sum_i Q_i C_i first, beta * Win added once
+                    o = make_double2(sign * o.x, sign * o.y);
+                    if (beta != 0.0) {
+                        const double2 wi = *reinterpret_cast<const double2*>(Win + r * M + b);
+                        o.x = beta * wi.x + o.x;
+                        o.y = beta * wi.y + o.y;
+                    }
                 }
                 *reinterpret_cast<double2*>(Wout + r * M + b) = o;
             }
@@ -260,10 +277,11 @@ update16_stream_kernel(const double* const* __restrict__ Qs, int d, const double
 template <int R, int NS>
 int launch_update16_stream(const double* const* Qs, int d, const double* C, const double* Win, double* Wout,
                            double beta, double sign, long long n, const int* live, cudaStream_t st) {
-    auto fn = update16_stream_kernel<R, NS>;
+    // short sums (d M <= 256) start the accumulators from beta * Win (see update_smem_kernel, dense.cu)
+    auto fn = d * 16 <= 256 ? update16_stream_kernel<R, NS, true> : update16_stream_kernel<R, NS, false>;
     constexpr size_t smem = sizeof(double) * (R * 16 + 256) * NS;
-    static int cache[kEkcgMaxDevices];
-    const int occ = kernel_occupancy(fn, 160, smem, cache);
+    static int cache[2][kEkcgMaxDevices];
+    const int occ = kernel_occupancy(fn, 160, smem, cache[d * 16 <= 256 ? 1 : 0]);
     if (occ < 1) return EKCG_EINVAL;
     const long long grid = (long long)occ * device_sms();
     const long long slabs = (n + R - 1) / R;

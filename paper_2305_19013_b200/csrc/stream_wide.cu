@@ -181,7 +181,7 @@ struct UpdWide {
     static_assert(M % 32 == 0, "octets of k-steps");
 };
 
-template <int M, int MR, int NS, int CW>
+template <int M, int MR, int NS, int CW, bool INIT>
 __global__ void __launch_bounds__(32 * (CW + 1))
 update_wide_stream_kernel(const double* const* __restrict__ Qs, int d, const double* __restrict__ C, const double* Win,
                           int ldwi, double* Wout, int ldwo, double beta, double sign, long long n,
@@ -194,9 +194,9 @@ update_wide_stream_kernel(const double* const* __restrict__ Qs, int d, const dou
     double* cs = sm + NS * P::SLAB;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const long long slabs = (n + R - 1) / R;
-    for (int e = threadIdx.x; e < d * M * M; e += blockDim.x) {
+    for (int e = threadIdx.x; e < d * M * M; e += blockDim.x) {  // INIT: sign * C, exact for sign = +-1
         const int i = e / (M * M), rem = e % (M * M);
-        cs[(i * M + rem / M) * LDC + rem % M] = C[e];
+        cs[(i * M + rem / M) * LDC + rem % M] = INIT ? sign * C[e] : C[e];
     }
     if (threadIdx.x == 0) {
 #pragma unroll
@@ -234,11 +234,24 @@ update_wide_stream_kernel(const double* const* __restrict__ Qs, int d, const dou
     for (long long sl = blockIdx.x; sl < slabs; sl += gridDim.x) {
         const long long rb = sl * R;
         const int rr = (int)min((long long)R, n - rb);
+        // the accumulators start from beta * Win (loads issued before the first ring wait), so the tile
+        // is stored straight from them after the K loop
         double acc[MR][NT][2];
 #pragma unroll
-        for (int mr = 0; mr < MR; ++mr)
+        for (int mr = 0; mr < MR; ++mr) {
+            const long long r = rb + warp * 8 * MR + 8 * mr + lc;
 #pragma unroll
-            for (int nt = 0; nt < NT; ++nt) acc[mr][nt][0] = acc[mr][nt][1] = 0.0;
+            for (int nt = 0; nt < NT; ++nt) {
+                double2 w = make_double2(0.0, 0.0);
+                if (INIT && beta != 0.0 && r < n) {
+                    w = *reinterpret_cast<const double2*>(Win + r * ldwi + 8 * nt + 2 * lr);
+                    w.x = beta * w.x;
+                    w.y = beta * w.y;
+                }
+                acc[mr][nt][0] = w.x;
+                acc[mr][nt][1] = w.y;
+            }
+        }
         for (int i = 0; i < d; ++i, ++t) {
             const int slot = (int)(t % NS);
             mbar_wait(&full[slot], (unsigned)((t / NS) & 1));
@@ -284,11 +297,14 @@ update_wide_stream_kernel(const double* const* __restrict__ Qs, int d, const dou
 #pragma unroll
             for (int nt = 0; nt < NT; ++nt) {
                 const int b = 8 * nt + 2 * lr;
-                double2 o = make_double2(sign * acc[mr][nt][0], sign * acc[mr][nt][1]);
-                if (beta != 0.0) {
-                    const double2 wi = *reinterpret_cast<const double2*>(Win + r * ldwi + b);
-                    o.x = beta * wi.x + o.x;
-                    o.y = beta * wi.y + o.y;
+                double2 o = make_double2(acc[mr][nt][0], acc[mr][nt][1]);
+                if (!INIT) {  // long sums: sign * sum_i Q_i C_i first, beta * Win added once
+                    o = make_double2(sign * o.x, sign * o.y);
+                    if (beta != 0.0) {
+                        const double2 wi = *reinterpret_cast<const double2*>(Win + r * ldwi + b);
+                        o.x = beta * wi.x + o.x;
+                        o.y = beta * wi.y + o.y;
+                    }
                 }
                 *reinterpret_cast<double2*>(Wout + r * ldwo + b) = o;
             }
@@ -316,7 +332,8 @@ template <int M, int MR, int NS, int CW>
 int launch_update_wide(const double* const* Qs, int d, const double* C, const double* Win, int ldwi, double* Wout,
                        int ldwo, double beta, double sign, long long n, const int* live, cudaStream_t st) {
     using P = UpdWide<M, MR, NS, CW>;
-    auto fn = update_wide_stream_kernel<M, MR, NS, CW>;
+    // short sums (d M <= 256) start the accumulators from beta * Win (see update_smem_kernel, dense.cu)
+    auto fn = d * M <= 256 ? update_wide_stream_kernel<M, MR, NS, CW, true> : update_wide_stream_kernel<M, MR, NS, CW, false>;
     const size_t smem = P::smem(d);
     if (smem > 227 * 1024) return EKCG_EINVAL;
     const int occ = resident_ctas(fn, smem, 32 * (CW + 1));

@@ -161,7 +161,8 @@ def test_pre_cholqr_breakdown_matches_reference(rng, m):
     n = 3000
     A, D = spd_csr(n, rng, 1.0, 100.0)
     U, _ = np.linalg.qr(rng.standard_normal((n, m)))
-    W = U * np.geomspace(1.0, 1e-10, m)
+    V, _ = np.linalg.qr(rng.standard_normal((m, m)))
+    W = (U * np.geomspace(1.0, 1e-10, m)) @ V.T  # mixed columns: unit scaling cannot undo it
     with pytest.raises(pk.Breakdown):
         pk.pre_cholqr(A, W)
     with pytest.raises(orc.OracleBreakdown):
