@@ -135,6 +135,7 @@ class DeviceEngine:
         self._slab, self._slab_off = None, 0
         # NVTX ranges per iteration and per tagged launch (host cost only when on)
         self.nvtx = os.environ.get("EKCG_NVTX", "0") == "1"
+        self.use_arena = True  # one allocation for all of a truncated window's blocks (see _setup)
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -145,9 +146,20 @@ class DeviceEngine:
         mm = self.m_max
         f64 = dict(dtype=torch.float64, device=dev)
         self.lean = self._choose_lean(n, mm)
-        self.WA = torch.empty(n * mm, **f64)
-        self.WB = torch.empty(0 if self.lean else n * mm, **f64)
-        self.WC = torch.empty(n * mm, **f64)
+        # Truncated windows: every n x m block of the solve (WA, WB, WC and the ring slots) is a slice of
+        # ONE allocation, so the caching allocator hands the same segment back to the next solve of the
+        # same size -- separately allocated 34 GB blocks fragment it (config 5: the second solve in a
+        # process could not find a 32 GiB hole in 31.5 GiB of free cache).
+        self._arena, self._arena_next = None, 0
+        if self.window is not None and self.use_arena:
+            nblk = (2 if self.lean else 3) + self.window * (1 if self.lean else 2)
+            self._arena = torch.empty(nblk * self._span(n * mm), **f64)
+            take = self._arena_block
+        else:
+            take = lambda numel: torch.empty(numel, **f64)  # noqa: E731
+        self.WA = take(n * mm)
+        self.WB = torch.empty(0, **f64) if self.lean else take(n * mm)
+        self.WC = take(n * mm)
         self.tmpv = torch.empty(n, **f64)
         self.tmpv2 = torch.empty(n, **f64)
         self.tmpv3 = torch.empty(n, **f64)
@@ -201,6 +213,16 @@ class DeviceEngine:
         cached = (2 * self.window + 3) * block + 6 * 8.0 * n
         free, _ = torch.cuda.mem_get_info(self.device)
         return cached > 0.92 * free
+
+    @staticmethod
+    def _span(numel):
+        return (numel + 31) // 32 * 32  # slices start on 256-B boundaries (TMA / 256-bit loads)
+
+    def _arena_block(self, numel):
+        """The next n x m_max slice of the solve's block arena."""
+        v = self._arena[self._arena_next:self._arena_next + numel]
+        self._arena_next += self._span(numel)
+        return v
 
     def _ensure(self, name, numel):
         buf = getattr(self, name)
@@ -310,8 +332,11 @@ class DeviceEngine:
             slot = self.since_clear % self.window
             if slot not in self.slots:
                 f64 = dict(dtype=torch.float64, device=self.device)
-                aq = None if self.lean else torch.empty(n * self.m_max, **f64)
-                self.slots[slot] = (torch.empty(n * self.m_max, **f64), aq)
+                take = self._arena_block if self._arena is not None else (
+                    lambda numel: torch.empty(numel, **f64))  # noqa: E731
+                q = take(n * self.m_max)
+                aq = None if self.lean else take(n * self.m_max)
+                self.slots[slot] = (q, aq)
             qbuf, aqbuf = self.slots[slot]
         else:
             slot = -1
@@ -716,10 +741,11 @@ class DeviceEngine:
         return max(1, min(lookahead, need))
 
     # ---------------------------------------------------------------- solve
-    def solve(self, b, x0=None, x_star=None, on_iteration=None):
+    def solve(self, b, x0=None, x_star=None, on_iteration=None, numpy_io=None):
+        """numpy_io: return x (and callback states) as numpy (default: when b is not a tensor)."""
         cfg = self.cfg
         dev = self.device
-        numpy_io = not isinstance(b, torch.Tensor)
+        numpy_io = (not isinstance(b, torch.Tensor)) if numpy_io is None else numpy_io
         self._setup()
         t_wall0 = time.perf_counter()
         ev0 = torch.cuda.Event(enable_timing=True)
@@ -818,7 +844,13 @@ class DeviceEngine:
         return true_res, rel
 
     def _output_x(self, numpy_io):
-        return self.x.cpu().numpy() if numpy_io else self.x
+        if not numpy_io:
+            return self.x
+        # into pinned host memory: torch's host caching allocator hands a freed result's pages to the next
+        # call, so a repeated 537 MB readback takes ~10 ms instead of ~250 ms of pageable page faults
+        out = torch.empty(self.x.numel(), dtype=torch.float64, pin_memory=True)
+        out.copy_(self.x)
+        return out.numpy()
 
     def _state(self, k, rho, tol1, numpy_io):
         conv = (lambda t: t.cpu().numpy()) if numpy_io else (lambda t: t.clone())

@@ -82,6 +82,7 @@ class ShardedEngine(DeviceEngine):
             local_op = CsrOperator(_LocalCsr(rp, vals, shard), device)
         self.decomposition = "layers" if self.stencil else ("subdomain" if self.order is not None else "rows")
         super().__init__(local_op, partition, cfg, device=device)
+        self.use_arena = False  # haloed blocks have their own (extended) sizes; _setup allocates them
         self.comm = comm
         self.shard = shard
         self.n_global = int(op.n)
@@ -255,7 +256,11 @@ class ShardedEngine(DeviceEngine):
             out = torch.empty_like(full)
             out[self._order_t.to(full.device)] = full
             full = out
-        return full.cpu().numpy() if numpy_io else full
+        if not numpy_io:
+            return full
+        out = torch.empty(full.numel(), dtype=torch.float64, pin_memory=True)  # see DeviceEngine._output_x
+        out.copy_(full)
+        return out.numpy()
 
     def _state(self, k, rho, tol1, numpy_io):
         raise NotImplementedError("on_iteration callbacks are not available on the sharded engine")

@@ -19,9 +19,13 @@ from paper_2305_19013_b200.problems import make_config  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--kmax", type=int, default=None)
 args = ap.parse_args()
 prob = make_config(args.config)
-cfg = pk.SolverConfig(**prob.solver_kwargs)
+kw = dict(prob.solver_kwargs)
+if args.kmax:
+    kw["kmax"] = args.kmax
+cfg = pk.SolverConfig(**kw)
 op = prob.stencil()
 b_dev = torch.as_tensor(prob.b, device="cuda")
 b_host = torch.from_numpy(np.ascontiguousarray(prob.b)).pin_memory()
@@ -33,7 +37,7 @@ def dev_solve():
 
 
 def host_solve():
-    return pk.enlarged_solve(op, b_host.numpy(), partition=prob.partition, cfg=cfg)
+    return pk.enlarged_solve(prob.stencil(), b_host.numpy(), partition=prob.partition, cfg=cfg)
 
 
 for f in (dev_solve, host_solve, dev_solve, host_solve):
