@@ -31,13 +31,13 @@ N5, N5Q, N3, N4 = 8192 ** 2, 4096 ** 2, 128 ** 3, 256 ** 3
 CASES = {
     "r02_cfg5full_hist_update": ("5 (8192^2, lean)", "hist_update", N5, 64, 3, 0, 0),
     "r02_cfg5full_stencil": ("5 (8192^2)", "stencil", N5, 64, 0, 5 * N5 - 4 * 8192, 512 * 512 * 8),
-    "r02_cfg5_hist_update": ("5 (4096^2)", "hist_update", N5Q, 64, 3, 0, 0),
+    "r02_cfg5full_hist_gram": ("5 (8192^2, lean)", "hist_gram", N5, 64, 3, 0, 0),
+    "r02_cfg5full_tri_apply": ("5 (8192^2, lean)", "tri_apply", N5, 64, 0, 0, 0),
     "r02_cfg5_hist_gram": ("5 (4096^2)", "hist_gram", N5Q, 64, 3, 0, 0),
-    "r02_cfg5_tri_apply": ("5 (4096^2)", "tri_apply", N5Q, 64, 0, 0, 0),
     "r02_cfg5_xr": ("5 (4096^2)", "xr", N5Q, 64, 0, 0, 0),
     "r02_cfg3_hist_update": ("3 (128^3)", "hist_update", N3, 32, 4, 0, 0),
     "r02_cfg3_hist_gram": ("3 (128^3)", "hist_gram", N3, 32, 4, 0, 0),
-    "r02_cfg3_stencil": ("3 (128^3)", "stencil", N3, 32, 0, 7 * N3 - 6 * 128 ** 2, 8 * 8 * 8),
+    "r02_cfg3_stencil": ("3 (128^3)", "stencil", N3, 32, 0, 7 * N3 - 6 * 128 ** 2, 8 * N3),
     "r02_cfg4_hist_update": ("4 (256^3)", "hist_update", N4, 64, 2, 0, 0),
     "r02_cfg4_hist_gram": ("4 (256^3)", "hist_gram", N4, 64, 2, 0, 0),
     "r02_cfg4_stencil": ("4 (256^3)", "stencil", N4, 64, 0, 7 * N4 - 6 * 256 ** 2, 0),
@@ -61,8 +61,8 @@ def main():
         dram = c["dram_gb"] * 1e9
         rows.append((cfg, tag, c["kernel"].replace("void <unnamed>::", "").replace("void ", ""), d, c["time_ms"],
                      b / 1e9, dram / 1e9, dram / b, hbm_frac, fp_frac, c.get("dmma_pipe_active", 0.0), bound))
-        if stem == "r02_cfg5full_hist_update":
-            traffic["cfg5-trunc3-srecg2-t64-tiled2d-8192, 8-iteration window from x0=0|hist_update"] = {
+        if stem in ("r02_cfg5full_hist_update", "r02_cfg5full_hist_gram", "r02_cfg5full_tri_apply"):
+            traffic[f"cfg5-trunc3-srecg2-t64-tiled2d-8192, 8-iteration window from x0=0|{tag}"] = {
                 "dram_bytes_per_launch": dram, "alg_bytes": b, "d": d, "time_ms": c["time_ms"],
                 "source": f"profiles/{stem}.ncu-rep (ncu --set full --clock-control none, one launch at d = {d})"}
     lines = ["# Round-2 ncu captures: one launch per hot kernel at steady-state depth d", "",
