@@ -101,6 +101,30 @@ def cfg3(k):
     })
 
 
+def cfg3_solve(edge):
+    """The complete config-3-class solve (to tol) by the real reference at a scaled edge: a reference
+    iteration count for the +-2 % criterion (the full 128^3 solve would take ~30 h here)."""
+    ref_src = os.environ.get("EKCG_REFERENCE", "/root/reference/pkg/src")
+    sys.path.insert(0, ref_src)
+    import ekcg  # the real reference
+    sys.path.insert(0, str(OUT))
+    from make_golden import config_inputs
+
+    A, b, _, part, kw = config_inputs(3, edge)
+    t1 = time.perf_counter()
+    _, rep = ekcg.enlarged_solve(A, b, partition=part, cfg=ekcg.SolverConfig(**kw))
+    wall = time.perf_counter() - t1
+    write(f"cfg3_solve{edge}", {
+        "source": "real reference ekcg.enlarged_solve (solvers.py:261-292), complete solve",
+        "config": f"cfg3-trunc4-srecg2-t32-skyscraper3d-128@{edge}", "edge": edge, "n": int(A.n), "cfg": kw,
+        "status": rep.status, "iterations": int(rep.iterations),
+        "residual_history": [float(v) for v in rep.residual_history],
+        "peak_block_vectors": int(rep.peak_block_vectors), "true_residual": float(rep.true_residual),
+        "b_sha256": arr_hash(b), "owner_sha256": arr_hash(part.owner()),
+        "csr_sha256": csr_hash(A.row_ptr, A.col_idx, A.values), "wall_s": wall, "host": host_info(),
+    })
+
+
 def lowmem(index, edge, k, chunk_rows):
     from oracle import ekcg_oracle as orc
     from paper_2305_19013_b200.problems import make_config
@@ -145,13 +169,15 @@ def lowmem(index, edge, k, chunk_rows):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("which", choices=["cfg3", "cfg4", "cfg5"])
+    ap.add_argument("which", choices=["cfg3", "cfg3solve", "cfg4", "cfg5"])
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--edge", type=int, default=None)
     ap.add_argument("--chunk-rows", type=int, default=1 << 18)
     args = ap.parse_args()
     if args.which == "cfg3":
         cfg3(args.k or 20)
+    elif args.which == "cfg3solve":
+        cfg3_solve(args.edge or 64)
     elif args.which == "cfg4":
         d = lowmem(4, args.edge, args.k or 10, args.chunk_rows)
         d["note"] = "s-step (s=4): no reference method exists (solvers.py:59); parity against the oracle's definition"

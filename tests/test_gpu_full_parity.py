@@ -95,3 +95,28 @@ def test_cfg4_full_size_vs_oracle():
 def test_cfg5_largest_oracle_instance():
     fx = _fixture("cfg5")
     _run(5, fx)
+
+
+def test_cfg3_class_complete_solve_iteration_count():
+    """The config-3 generator at 64^3 solved to tol by the real reference (full_cfg3_solve64.json):
+    iteration count within +-2 % (north star), history over k <= 20 within 1e-8, true residual <= tol.
+    (The full 128^3 reference solve would take ~30 h on the build host, so its count is not pinned.)"""
+    p = GOLDEN / "full_cfg3_solve64.json"
+    if not p.exists():
+        pytest.skip("full_cfg3_solve64.json not generated")
+    fx = json.loads(p.read_text())
+    prob = make_config(3, fx["edge"])
+    assert _sha(prob.b) == fx["b_sha256"] and _sha(prob.partition.owner()) == fx["owner_sha256"]
+    x, rep = pk.enlarged_solve(prob.stencil(), prob.b, partition=prob.partition,
+                               cfg=pk.SolverConfig(**prob.solver_kwargs))
+    it_ref = fx["iterations"]
+    print(f"cfg3@{fx['edge']}: {rep.iterations} iterations (reference {it_ref}), true residual "
+          f"{rep.true_residual / np.linalg.norm(prob.b):.2e}")
+    assert rep.status == fx["status"] == "converged"
+    assert abs(rep.iterations - it_ref) <= max(1, round(0.02 * it_ref))
+    h, g = np.asarray(rep.residual_history), np.asarray(fx["residual_history"])
+    k = min(len(h), len(g), 21)
+    assert np.max(np.abs(h[:k] / h[0] - g[:k] / g[0]) / (g[:k] / g[0])) <= HIST_TOL
+    # the stop test is on the recurrence residual; the true one is reported (solvers.py:289): hold it to tol,
+    # or to the reference's own final true residual when that one already ends above tol
+    assert rep.true_residual <= max(1e-8 * np.linalg.norm(prob.b), 1.5 * fx["true_residual"])
