@@ -112,12 +112,14 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
     const int quad = warp / KS;
     const int a_base = (quad % QA) * TA * 8;
     const int b_base = (quad / QA) * TB * 8;
-    const int i0 = blockIdx.y * GB;
+    // grid (block groups, chunks): the CTAs of one row chunk are consecutive, so the groups that read the
+    // same Y rows run together and share them through L2 instead of re-reading Y from HBM per group
+    const int i0 = blockIdx.x * GB;
     const int nb = min(GB, d - i0);
     const double* __restrict__ X[GB];
 #pragma unroll
     for (int g = 0; g < GB; ++g) X[g] = Xs[min(i0 + g, d - 1)];
-    const long long r0 = blockIdx.x * rows_chunk;
+    const long long r0 = blockIdx.y * rows_chunk;
     long long r1 = r0 + rows_chunk;
     if (r1 > n) r1 = n;
     const long long steps = (r1 > r0) ? (r1 - r0 + 3) / 4 : 0;
@@ -164,7 +166,7 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
 #pragma unroll
         for (int g = 0; g < GB; ++g) {
             if (g >= nb) break;
-            double* out = partials + ((long long)blockIdx.x * d + i0 + g) * (M * M);
+            double* out = partials + ((long long)blockIdx.y * d + i0 + g) * (M * M);
 #pragma unroll
             for (int ta = 0; ta < TA; ++ta)
 #pragma unroll
@@ -196,7 +198,7 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
             double s = red[g * M * M + e];
 #pragma unroll
             for (int k = 1; k < KS; ++k) s += red[(k * GB + g) * M * M + e];
-            partials[((long long)blockIdx.x * d + i0 + g) * (M * M) + e] = s;
+            partials[((long long)blockIdx.y * d + i0 + g) * (M * M) + e] = s;
         }
     }
 }
@@ -928,7 +930,7 @@ extern "C" int ekcg_gram(const double* const* Xs, int ldx, int d, int m1, const 
     } else if (fn != nullptr && launch_gram_stream(Xs, ldx, d, m1, Y, ldy, m2, n, chunks, rc, partials, live, st) == EKCG_OK) {
         // streamed (TMA bulk) Gram, stream.cu
     } else if (fn != nullptr) {
-        launch_k(fn, grid, kGramThreads, 0, st, Xs, ldx, d, Y, ldy, n, rc, partials, live);
+        launch_k(fn, dim3(grid.y, grid.x), kGramThreads, 0, st, Xs, ldx, d, Y, ldy, n, rc, partials, live);
     } else {
         const int O = m1 * m2;
         size_t smem = (O <= 256) ? sizeof(double) * 256 : 0;

@@ -1,5 +1,5 @@
 for rep in 1 2; do
-for lib in tools/lib_base.so tools/lib_init4.so; do
+for lib in tools/lib_base.so tools/lib_swap.so; do
   timeout 120 python tools/kbench_cgs2.py $lib 262144 16 100 inplace 2>&1 | tail -1
   timeout 120 python tools/kbench_cgs2.py $lib 262144 16 8 inplace 2>&1 | tail -1
   timeout 120 python tools/kbench_cgs2.py $lib 2097152 32 4 inplace 2>&1 | tail -1
