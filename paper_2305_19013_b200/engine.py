@@ -126,11 +126,12 @@ class DeviceEngine:
             if not self.pc_aligned:
                 self.notes_init.append("preconditioner blocks not aligned with partition subdomains; "
                                        "using explicit split application")
-        # replay steady-state iterations of truncated windows from CUDA graphs
-        # (one per ring phase; iteration numbers are read on the device).  Off by
-        # default: measured on config 1, capture costs more than the direct
-        # launches it replaces (15 ms per 130-iteration solve without graphs).
-        self.use_graphs = False
+        # replay steady-state iterations of truncated windows from CUDA graphs (one per ring
+        # phase; iteration numbers are read on the device).  "auto": for small blocks
+        # (n m <= 2^20), where the Python enqueue of an iteration (~80 us) is as long as the
+        # GPU's (~84 us at config 1) and the queue would drain at batch boundaries; a replay
+        # costs ~10 us of host time.  Large blocks gain nothing from it.
+        self.use_graphs = "auto"
         self._capturing = False
         self._slab, self._slab_off = None, 0
         # NVTX ranges per iteration and per tagged launch (host cost only when on)
@@ -237,7 +238,8 @@ class DeviceEngine:
         return -1 if self._capturing else k
 
     def _graph_eligible(self):
-        return (self.use_graphs and self.kernel_timer is None and self.window is not None
+        want = (self.n * self.m_max <= (1 << 20)) if self.use_graphs == "auto" else bool(self.use_graphs)
+        return (want and self.kernel_timer is None and self.window is not None
                 and self.retention == "trunc" and self.cfg.switch_tol is None
                 and self.method in ("sre-cg2", "sre-cg") and self.kmax + 1 <= self.history.numel())
 

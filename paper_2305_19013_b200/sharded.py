@@ -83,6 +83,7 @@ class ShardedEngine(DeviceEngine):
         self.decomposition = "layers" if self.stencil else ("subdomain" if self.order is not None else "rows")
         super().__init__(local_op, partition, cfg, device=device)
         self.use_arena = False  # haloed blocks have their own (extended) sizes; _setup allocates them
+        self.use_graphs = False  # iterations issue collectives: no graph capture
         self.comm = comm
         self.shard = shard
         self.n_global = int(op.n)

@@ -59,6 +59,7 @@ def _single(name):
         op = pk.CsrOperator(op, dev)
     eng = DeviceEngine(op, prob.partition, cfg, device=dev)
     eng.cache_aq = {"cached": True, "lean": False}[scheme]
+    eng.fuse_prechol_max = 0  # the sharded engine runs update2, Graw and the factor as separate kernels
     x, rep = eng.solve(prob.b, x_star=prob.x_star)
     return x, rep
 
