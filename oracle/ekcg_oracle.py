@@ -335,24 +335,36 @@ def run_oracle(row_ptr, col_idx, values, b, owner, t, *, method="sre-cg2", s=1,
 # run_oracle on small problems with many chunks.
 # ---------------------------------------------------------------------------
 
-def csr_spmm_chunked(row_ptr, col_idx, values, X, chunk_rows, out=None):
-    """csr_spmm / csr_spmv over row chunks (bitwise the same as the unchunked forms)."""
+def csr_spmm_chunked(row_ptr, col_idx, values, X, chunk_rows, out=None, threads=None):
+    """csr_spmm / csr_spmv over row chunks (bitwise the same as the unchunked forms).
+    Chunks are independent, so `threads` > 1 runs them on a thread pool (numpy
+    releases the GIL inside the gather / multiply / reduceat loops)."""
     n = row_ptr.shape[0] - 1
     vec = X.ndim == 1
     Y = out if out is not None else np.empty(X.shape)
-    for a in range(0, n, chunk_rows):
+
+    def one(a):
         b = min(n, a + chunk_rows)
         lo, hi = int(row_ptr[a]), int(row_ptr[b])
         rp = row_ptr[a:b + 1] - lo
         if vec:
             Y[a:b] = csr_spmv(rp, col_idx[lo:hi], values[lo:hi], X)
-        else:
-            m = X.shape[1]
-            scale = values[lo:hi, None]
-            ci = col_idx[lo:hi]
-            for c0 in range(0, m, COLUMN_SLAB):
-                c1 = min(m, c0 + COLUMN_SLAB)
-                Y[a:b, c0:c1] = np.add.reduceat(scale * X[ci, c0:c1], rp[:-1], axis=0)
+            return
+        m = X.shape[1]
+        scale = values[lo:hi, None]
+        ci = col_idx[lo:hi]
+        for c0 in range(0, m, COLUMN_SLAB):
+            c1 = min(m, c0 + COLUMN_SLAB)
+            Y[a:b, c0:c1] = np.add.reduceat(scale * X[ci, c0:c1], rp[:-1], axis=0)
+
+    starts = range(0, n, chunk_rows)
+    if threads and threads > 1 and len(starts) > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(threads) as ex:
+            list(ex.map(one, starts))
+    else:
+        for a in starts:
+            one(a)
     return Y
 
 
@@ -377,7 +389,7 @@ def _tri_solve_inplace(W, R, chunk_rows):
 
 def run_oracle_lowmem(row_ptr, col_idx, values, b, owner, t, *, method="sre-cg2", s=1, tol=1e-8, kmax=None,
                       retention="trunc", trunc=None, true_residual_every=50, chunk_rows=1 << 18,
-                      on_iteration=None):
+                      on_iteration=None, threads=None):
     """run_oracle for unpreconditioned SRE-CG2 / SRE-CG (s >= 1, full or truncated
     retention) holding only the retained Q blocks, the candidate and one scratch
     block: what lets the config-4 (256^3, n x 64) fixture run on a 62 GB host."""
@@ -390,7 +402,7 @@ def run_oracle_lowmem(row_ptr, col_idx, values, b, owner, t, *, method="sre-cg2"
     owner = np.asarray(owner, dtype=np.int64)
     n = b.shape[0]
     cr = int(chunk_rows)
-    op = lambda X, out=None: csr_spmm_chunked(row_ptr, col_idx, values, X, cr, out)  # noqa: E731
+    op = lambda X, out=None: csr_spmm_chunked(row_ptr, col_idx, values, X, cr, out, threads)  # noqa: E731
     window = 2 if method == "sre-cg" else (trunc if retention == "trunc" else None)
     kmax = kmax if kmax is not None else 2 * n
 
