@@ -125,7 +125,7 @@ def cfg3_solve(edge):
     })
 
 
-def lowmem(index, edge, k, chunk_rows):
+def lowmem(index, edge, k, chunk_rows, threads=None):
     from oracle import ekcg_oracle as orc
     from paper_2305_19013_b200.problems import make_config
 
@@ -146,7 +146,7 @@ def lowmem(index, edge, k, chunk_rows):
         print(f"  k={state['k']} rho={state['rho']:.6e} t={stamps[-1] - t1:.1f}s", flush=True)
 
     out = orc.run_oracle_lowmem(A.row_ptr, A.col_idx, A.values, prob.b, owner, t, chunk_rows=chunk_rows,
-                                on_iteration=on_it, **kw)
+                                on_iteration=on_it, threads=threads, **kw)
     wall = time.perf_counter() - t1
     kw["t"] = t
     d = {
@@ -173,18 +173,19 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--edge", type=int, default=None)
     ap.add_argument("--chunk-rows", type=int, default=1 << 18)
+    ap.add_argument("--threads", type=int, default=None, help="thread pool for the row-chunked SpMM")
     args = ap.parse_args()
     if args.which == "cfg3":
         cfg3(args.k or 20)
     elif args.which == "cfg3solve":
         cfg3_solve(args.edge or 64)
     elif args.which == "cfg4":
-        d = lowmem(4, args.edge, args.k or 10, args.chunk_rows)
+        d = lowmem(4, args.edge, args.k or 10, args.chunk_rows, args.threads)
         d["note"] = "s-step (s=4): no reference method exists (solvers.py:59); parity against the oracle's definition"
         write("cfg4", d)
     else:
         edge = args.edge or 4096
-        d = lowmem(5, edge, args.k or 12, args.chunk_rows)
+        d = lowmem(5, edge, args.k or 12, args.chunk_rows, args.threads)
         if edge != 8192:
             d["note"] = (f"largest config-5 instance the bounded-memory oracle fits in this host's 62 GB "
                          f"({edge}^2 of 8192^2; one full-size n x 64 block is 34.4 GB)")
