@@ -241,6 +241,31 @@ int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx, double* Y
                     int k, int kmax, int stagnation_window, double* history, int do_finish, double* rho2_out,
                     void* stream);
 
+/* ---- whole solve in one kernel (small problems) ------------------------- */
+
+/* The complete truncated-window SRE-CG / SRE-CG2 loop of `_run_engine`
+ * (solvers.py:319-428: candidate, CGS2 aortho.py:89-95, Pre-CholQR + A-CholQR
+ * aortho.py:98-110, alpha / x / r update and stop test solvers.py:394-415, the
+ * true-residual log every `every` iterations :401-402) as ONE kernel on one
+ * thread-block cluster (up to 16 CTAs, distributed-shared-memory reductions,
+ * hardware cluster barriers): for problems whose blocks live in L2, where an
+ * iteration of separate launches is latency-bound.  Unpreconditioned, s = 1,
+ * t <= 16, window * t^2 <= 512; the operator is the stencil `desc` (whole
+ * grid) or, with desc == NULL, a CSR matrix whose rows hold at most 8 entries.
+ * Before the call: x = x0, r = b - A x0, and ctrl / history[0] initialised by
+ * ekcg_start.  `blocks` is scratch of (2 window + 3) * span + n doubles (span >=
+ * n t, a multiple of 32).  On return (stream order) ctrl holds the final
+ * status / k_done / breakdown record, history[1..k_done] the residual norms,
+ * checks[j] the true residual after iteration (j + 1) * every.  phase_ticks (may
+ * be NULL) is a diagnostic: 20 device int64 that CTA 0 increments by the SM cycles
+ * it spent in each phase of the iteration (tools/cluster_time.py names them). */
+int ekcg_cluster_solve_fits(long long n, int t, int window);
+int ekcg_cluster_solve(const EkcgStencil* desc, const long long* row_ptr, const int* col_idx,
+                       const double* values, long long n, int t, int window, int kmax, int every,
+                       const int* owner, const double* b, double* x, double* r, double* blocks,
+                       long long span, void* ctrl, double* history, double* checks, double chol_tol,
+                       long long* phase_ticks, void* stream);
+
 /* ---- engine bookkeeping ------------------------------------------------ */
 
 /* Size in bytes of the control block. */

@@ -15,7 +15,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libekcg_b200.so"
-SOURCES = ["sparse.cu", "stencil_march.cu", "stream.cu", "stream_wide.cu", "dense.cu", "small.cu", "fused.cu"]
+SOURCES = ["sparse.cu", "stencil_march.cu", "stream.cu", "stream_wide.cu", "dense.cu", "small.cu", "fused.cu", "cluster_solve.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -137,6 +137,13 @@ class DeviceEngine:
         # NVTX ranges per iteration and per tagged launch (host cost only when on)
         self.nvtx = os.environ.get("EKCG_NVTX", "0") == "1"
         self.use_arena = True  # one allocation for all of a truncated window's blocks (see _setup)
+        # whole solve in one thread-block-cluster kernel (csrc/cluster_solve.cu) for small
+        # truncated-window problems: "auto" (n m <= 2^18, where an iteration of separate
+        # launches is latency-bound), True (whenever the kernel applies) or False
+        self.use_cluster = "auto"
+        self.cluster_ok = True  # False in the sharded engine
+        self.ran_cluster = False
+        self.cluster_ticks = None  # optional int64[20] device tensor: per-phase SM cycles of CTA 0
 
     # ------------------------------------------------------------------ setup
     def _setup(self):
@@ -757,6 +764,12 @@ class DeviceEngine:
 
         sync_each = (on_iteration is not None or self.retention == "restart-tol"
                      or cfg.switch_tol is not None or self.sync_mode)
+        if not sync_each and self._cluster_eligible():
+            ctrl = self._solve_cluster()
+            ev1.record()
+            ev1.synchronize()
+            solve_s = ev0.elapsed_time(ev1) / 1e3
+            return self._report(ctrl, x_star, numpy_io, solve_s, time.perf_counter() - t_wall0)
         host_hist = None
         if sync_each:
             c = self._read_ctrl()
@@ -815,6 +828,56 @@ class DeviceEngine:
         ev1.synchronize()
         solve_s = ev0.elapsed_time(ev1) / 1e3
         return self._report(ctrl, x_star, numpy_io, solve_s, time.perf_counter() - t_wall0)
+
+    # -------------------------------------------------------- cluster solve
+    def _cluster_eligible(self):
+        """The one-kernel cluster solve (csrc/cluster_solve.cu) covers unpreconditioned SRE-CG /
+        SRE-CG2 with a truncation window, s = 1, t <= 16, window t^2 <= 512, on a whole-grid
+        stencil operator or a CSR matrix with rows of at most 8 entries."""
+        from .operators import CsrOperator, StencilOperator
+        if not self.cluster_ok or self.use_cluster is False or self.kernel_timer is not None or self.no_fuse:
+            return False
+        if (self.method not in ("sre-cg2", "sre-cg") or self.s != 1 or self.retention != "trunc"
+                or self.pc is not None or self.norm_pc is not None or self.cfg.switch_tol is not None
+                or self.lean or self.window is None or self.kmax + 1 > self.history.numel()):
+            return False
+        t = self.t_cur
+        if not _lib.query("ekcg_cluster_solve_fits", self.n, t, self.window):
+            return False
+        if self.use_cluster == "auto" and self.n * t > (1 << 18):
+            return False
+        op = self.op
+        if isinstance(op, StencilOperator):
+            return True
+        if isinstance(op, CsrOperator):
+            if not hasattr(op, "_max_row"):
+                op._max_row = int((op.row_ptr[1:] - op.row_ptr[:-1]).max().item()) if self.n else 0
+            return op._max_row <= 8
+        return False
+
+    def _solve_cluster(self):
+        """Run the whole solve in the cluster kernel; returns the final control block."""
+        from .operators import StencilOperator
+        n, t, w = self.n, self.t_cur, self.window
+        span = self._span(n * t)
+        blocks = torch.empty((2 * w + 3) * span + self._span(n), dtype=torch.float64, device=self.device)
+        nchk = max(1, self.kmax // self.every + 1)
+        self._ensure_checks(nchk)
+        op = self.op
+        if isinstance(op, StencilOperator):
+            desc, rp, ci, vv = op.desc_ref(), None, None, None
+        else:
+            desc, rp, ci, vv = None, op.row_ptr.data_ptr(), op.col_idx.data_ptr(), op.values.data_ptr()
+        _lib.call("ekcg_cluster_solve", desc, rp, ci, vv, n, t, w, self.kmax, self.every,
+                  self.owner_dev.data_ptr(), self.b.data_ptr(), self.x.data_ptr(), self.r.data_ptr(),
+                  blocks.data_ptr(), span, self.ctrl.data_ptr(), self.history.data_ptr(), self.checks.data_ptr(),
+                  1e-14, None if self.cluster_ticks is None else self.cluster_ticks.data_ptr(), self.stream)
+        ctrl = self._read_ctrl()
+        self._cluster_blocks = blocks
+        self.ran_cluster = True
+        last = ctrl["k_done"] + (1 if ctrl["status"] == 3 else 0)
+        self.launch_k = [(k, min(k - 1, w), t) for k in range(1, last + 1)]
+        return ctrl
 
     def _begin(self, b, x0):
         """Upload b / x0, r = b - A x, rho0 = |r| and the control block (solvers.py:341-345)."""

@@ -84,6 +84,7 @@ class ShardedEngine(DeviceEngine):
         super().__init__(local_op, partition, cfg, device=device)
         self.use_arena = False  # haloed blocks have their own (extended) sizes; _setup allocates them
         self.use_graphs = False  # iterations issue collectives: no graph capture
+        self.cluster_ok = False  # the one-kernel cluster solve is a single-GPU path
         self.comm = comm
         self.shard = shard
         self.n_global = int(op.n)

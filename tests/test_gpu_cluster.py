@@ -1,0 +1,159 @@
+"""The one-kernel cluster solve (csrc/cluster_solve.cu, `ekcg_cluster_solve`): the whole
+truncated-window loop of `_run_engine` (solvers.py:319-428) on one thread-block cluster.
+
+Checked against the real reference's goldens (history 1e-8 over k <= 20, iteration count,
+status, peak, true-residual log), against the launch-per-phase engine on the same inputs,
+and for bit-identical reruns (fixed-order reductions, no atomics).
+"""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_2305_19013_b200 as pk
+from paper_2305_19013_b200.engine import DeviceEngine
+from paper_2305_19013_b200.problems import make_config
+from paper_2305_19013_b200.solvers import SolverConfig
+from conftest import golden_case_inputs
+from test_gpu_solver import hist_dev, hist_tol, iter_tol
+
+
+def _engines(op, partition, cfg, b, x0=None, x_star=None):
+    out = []
+    for use in (True, False):
+        eng = DeviceEngine(op, partition, cfg)
+        eng.use_cluster = use
+        x, rep = eng.solve(b, x0, x_star=x_star)
+        assert eng.ran_cluster == use, "wrong engine path"
+        out.append((x, rep))
+    return out
+
+
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+def test_cfg1_cluster_matches_reference(solves_golden, floors_golden, form):
+    """BASELINE config 1 (SRE-CG, t = 8, 100^2 Poisson) against the real reference's run."""
+    meta, arrays = solves_golden
+    name = "cfg1_100"
+    prob = make_config(1, 100)
+    op = prob.stencil() if form == "stencil" else prob.csr()
+    eng = DeviceEngine(op, prob.partition, SolverConfig(**prob.solver_kwargs))
+    x, rep = eng.solve(prob.b, x_star=prob.x_star)
+    assert eng.ran_cluster, "config 1 should take the cluster kernel"
+    ref = meta[name]
+    assert rep.status == ref["status"] == "converged"
+    assert hist_dev(rep.residual_history, arrays[f"{name}__history"]) <= hist_tol(floors_golden, name)
+    assert abs(rep.iterations - ref["iterations"]) <= iter_tol(floors_golden, name, ref["iterations"])
+    assert rep.peak_block_vectors == ref["peak_block_vectors"]
+    assert [c[0] for c in rep.true_residual_checks] == [c[0] for c in ref["true_residual_checks"]]
+    for (_, got), (_, want) in zip(rep.true_residual_checks, ref["true_residual_checks"]):
+        assert abs(got - want) <= 1e-6 * want + 1e-12
+    assert rep.true_residual <= 1e-8 * np.linalg.norm(prob.b) * 10
+    assert rep.relative_error is not None and rep.relative_error < 1e-6
+
+
+CASES = [  # (config class, edge, solver overrides)
+    (1, 40, {}),
+    (1, 64, {"method": "sre-cg2", "retention": "trunc", "trunc": 3}),
+    (2, 12, {"retention": "trunc", "trunc": 2}),          # 3-D, t = 16: 8-CTA cluster (receive buffers)
+    (2, 10, {"method": "sre-cg"}),
+    (1, 33, {"method": "sre-cg2", "retention": "trunc", "trunc": 4, "true_residual_every": 7}),
+]
+
+
+@pytest.mark.parametrize("idx,edge,over", CASES)
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+def test_cluster_matches_launch_per_phase_engine(idx, edge, over, form):
+    prob = make_config(idx, edge)
+    cfg = SolverConfig(**dict(prob.solver_kwargs, **over))
+    op = prob.stencil() if form == "stencil" else prob.csr()
+    (xa, a), (xb, b) = _engines(op, prob.partition, cfg, prob.b, x_star=prob.x_star)
+    assert a.status == b.status == "converged"
+    assert abs(a.iterations - b.iterations) <= max(1, round(0.02 * b.iterations))
+    assert hist_dev(a.residual_history, b.residual_history) <= 1e-9
+    assert a.peak_block_vectors == b.peak_block_vectors or a.iterations != b.iterations
+    assert [c[0] for c in a.true_residual_checks][:3] == [c[0] for c in b.true_residual_checks][:3]
+    assert np.linalg.norm(xa - xb) <= 1e-6 * np.linalg.norm(xb)
+
+
+def test_cluster_tile_field_operator():
+    """Variable-coefficient (kappa tile field) stencil rows inside the cluster kernel."""
+    from paper_2305_19013_b200.partition import Partition
+    rng = np.random.default_rng(11)
+    nx = ny = 48
+    field = np.exp(rng.uniform(-2.0, 2.0, size=(ny // 8, nx // 8)))
+    op = pk.StencilOperator((nx, ny), kappa=field, tile=(8, 8))
+    owner = (np.arange(ny)[:, None] // (ny // 4) * 2 + np.arange(nx)[None, :] // (nx // 2)).reshape(-1)
+    part = Partition.from_owner(owner.astype(np.int64), 8)
+    b = rng.uniform(-1.0, 1.0, nx * ny)
+    cfg = SolverConfig(method="sre-cg2", t=8, tol=1e-8, retention="trunc", trunc=3)
+    (xa, a), (xb, b_) = _engines(op, part, cfg, b)
+    assert a.status == b_.status == "converged"
+    assert abs(a.iterations - b_.iterations) <= max(1, round(0.02 * b_.iterations))
+    assert hist_dev(a.residual_history, b_.residual_history) <= 1e-9
+    # and the CSR form of the same operator
+    A = op.to_csr()
+    eng = DeviceEngine(A, part, cfg)
+    eng.use_cluster = True
+    xc, c = eng.solve(b)
+    assert eng.ran_cluster
+    assert np.array_equal(c.residual_history, a.residual_history), "stencil and CSR rows are bitwise the same operator"
+
+
+def test_cluster_rerun_bit_identical():
+    prob = make_config(1, 100)
+    cfg = SolverConfig(**prob.solver_kwargs)
+    outs = []
+    for _ in range(3):
+        eng = DeviceEngine(prob.stencil(), prob.partition, cfg)
+        x, rep = eng.solve(prob.b)
+        assert eng.ran_cluster
+        outs.append((x, rep.residual_history))
+    for x, h in outs[1:]:
+        assert np.array_equal(x, outs[0][0]) and np.array_equal(h, outs[0][1])
+
+
+def test_cluster_breakdown_and_maxiter(solves_golden):
+    """The p12_srecg2_t8_trunc2 golden breaks down at iteration 17; kmax stops report maxiter."""
+    meta, arrays = solves_golden
+    name = "p12_srecg2_t8_trunc2"
+    rp, ci, vals, b, owner, x0 = golden_case_inputs(arrays, name)
+    A = pk.SparseSpdMatrix(len(rp) - 1, rp, ci, vals)
+    kw = dict(meta[name]["cfg"])
+    part = pk.Partition.from_owner(owner, kw["t"])
+    eng = DeviceEngine(A, part, SolverConfig(**kw))
+    x, rep = eng.solve(b, x0)
+    assert eng.ran_cluster
+    ref = meta[name]
+    assert rep.status == ref["status"] == "breakdown"
+    assert rep.iterations == ref["iterations"]
+    assert rep.notes[0].split(":")[0] == ref["notes"][0].split(":")[0]
+    eng = DeviceEngine(A, part, SolverConfig(**dict(kw, kmax=5)))
+    x, rep = eng.solve(b, x0)
+    assert eng.ran_cluster and rep.status == "maxiter" and rep.iterations == 5
+    assert len(rep.residual_history) == 6
+
+
+def test_cluster_x0_and_torch_io():
+    prob = make_config(1, 40)
+    cfg = SolverConfig(**prob.solver_kwargs)
+    rng = np.random.default_rng(3)
+    x0 = rng.standard_normal(prob.n)
+    (xa, a), (xb, b) = _engines(prob.stencil(), prob.partition, cfg, prob.b, x0=x0)
+    assert a.status == b.status == "converged"
+    assert hist_dev(a.residual_history, b.residual_history) <= 1e-9
+    bt = torch.as_tensor(prob.b, device="cuda")
+    x, rep = pk.enlarged_solve(prob.stencil(), bt, partition=prob.partition, cfg=cfg)
+    assert isinstance(x, torch.Tensor) and x.is_cuda and rep.status == "converged"
+
+
+def test_cluster_not_taken_when_ineligible():
+    prob = make_config(3, 16)  # t = 32
+    eng = DeviceEngine(prob.stencil(), prob.partition, SolverConfig(**dict(prob.solver_kwargs, kmax=5)))
+    eng.solve(prob.b)
+    assert not eng.ran_cluster
+    prob = make_config(2, 12)  # full retention
+    eng = DeviceEngine(prob.stencil(), prob.partition, SolverConfig(**dict(prob.solver_kwargs, kmax=5)))
+    eng.solve(prob.b)
+    assert not eng.ran_cluster

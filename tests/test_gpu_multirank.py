@@ -60,6 +60,7 @@ def _single(name):
     eng = DeviceEngine(op, prob.partition, cfg, device=dev)
     eng.cache_aq = {"cached": True, "lean": False}[scheme]
     eng.fuse_prechol_max = 0  # the sharded engine runs update2, Graw and the factor as separate kernels
+    eng.use_cluster = False   # ... one launch per phase
     x, rep = eng.solve(prob.b, x_star=prob.x_star)
     return x, rep
 

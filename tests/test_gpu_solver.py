@@ -319,6 +319,7 @@ def test_sharded_engine_single_rank_matches(idx, edge, over, form):
     op = prob.stencil() if form == "stencil" else prob.csr()
     single = DeviceEngine(op, prob.partition, cfg)
     single.fuse_prechol_max = 0  # the sharded engine does not fuse update2 + Graw + factor
+    single.use_cluster = False   # ... and launches per phase (same kernel sequence)
     _, ref = single.solve(prob.b, x_star=prob.x_star)
     x, rep = ShardedEngine(op, prob.partition, cfg).solve(prob.b, x_star=prob.x_star)
     assert rep.status == ref.status
@@ -342,6 +343,7 @@ def test_graph_replay_matches_direct_launches(idx, edge):
     for graphs in (True, False):
         eng = DeviceEngine(op, prob.partition, cfg)
         eng.use_graphs = graphs
+        eng.use_cluster = False  # the launch-per-phase engine is what graphs replay
         x, rep = eng.solve(prob.b)
         reps.append((x, rep, eng))
     (xa, a, ea), (xb, b, eb) = reps
