@@ -275,11 +275,25 @@ int launch_march(const EkcgStencil& s, const UniformFaces& uf, const double* X, 
                                        : (long long)((s.nx + P::TX - 1) / P::TX);
     const int colchunks = (m + KC - 1) / KC;
     const long long per_chunk = tiles * colchunks;
-    // enough CTAs for two waves of the resident slots; a march of at least 8 planes
-    long long wchunks = (2LL * resident + per_chunk - 1) / per_chunk;
+    // Split the march axis into w chunks so that the grid fills whole waves of the resident slots:
+    // the launch takes about waves(w) x (planes per CTA + the 2 halo planes each chunk re-reads), so a
+    // grid of 2.6 waves (what "two waves, rounded up" gave configs 3 and 5) idles 14 % of the slot-time
+    // in its last wave.  Marches of at least 8 planes; ties go to the finer split.
     const int planes = we - wb;
-    if (wchunks > planes / 8) wchunks = planes / 8;
-    if (wchunks < 1) wchunks = 1;
+    long long wmax = planes / 8;
+    if (wmax < 1) wmax = 1;
+    if (wmax > 64) wmax = 64;
+    long long wchunks = 1, best_cost = -1;
+    for (long long w = 1; w <= wmax; ++w) {
+        const long long per_cta = (planes + w - 1) / w;
+        const long long ctas = per_chunk * ((planes + per_cta - 1) / per_cta);
+        const long long waves = (ctas + resident - 1) / resident;
+        const long long cost = waves * (per_cta + 2);
+        if (best_cost < 0 || cost <= best_cost) {
+            best_cost = cost;
+            wchunks = w;
+        }
+    }
     const int wchunk = (int)((planes + wchunks - 1) / wchunks);
     dim3 grid((unsigned)tiles, colchunks, (planes + wchunk - 1) / wchunk);
     launch_k(stencil_march_kernel<P>, grid, P::NT, P::SMEM, st, map, s, uf, Y, ldy, m, wb, we, wchunk, live);
