@@ -204,68 +204,65 @@ __device__ __forceinline__ void apply_items(const Args& a, const double* X, int 
         const unsigned rl = pow2 ? (it >> sh) : it / groups;
         const long long row = r0 + rl;
         const int c = (int)(it - rl * groups) * VW;
-        if (!CSR && a.s.kfield == nullptr) {
-            // constant-kappa grid, interior node: fixed offsets and the precomputed uniform faces
-            // (the values stencil_row would produce, in the same entry order)
-            const unsigned nx = a.s.nx, ny = a.s.ny, nz = a.s.nz;
+        if (!CSR) {
+            // grid stencil: coefficients in slot order z-, y-, x-, diag, x+, y+, z+ with a presence mask
+            // (stencil_coef: uniform faces, tile field or per-node table), fixed neighbour offsets, every
+            // present entry loaded up front, then p0 + (((p1 + p2) + ...)) over the present entries in
+            // order -- no per-row branches, so interior and boundary rows of a warp take the same path
+            const unsigned nx = a.s.nx, ny = a.s.ny;
             const unsigned iu = (unsigned)row;
             const unsigned x = iu % nx, rest = iu / nx;
             const bool three = a.s.dim == 3;
-            const unsigned y = three ? rest % ny : rest, z = three ? rest / ny : 1u;
-            if (x > 0 && x + 1 < nx && y > 0 && y + 1 < ny && (!three || (z > 0 && z + 1 < nz))) {
-                const double* xc = X + row * ldx + c;
-                const long long sy = (long long)nx * ldx, sz = sy * ny;
-                double v[7][VW];
-                auto ld = [&](const double* src, double (&o)[VW]) {
+            const unsigned y = three ? rest % ny : rest, z = three ? rest / ny : 0u;
+            double cf[7];
+            const unsigned mk = stencil_coef(a.s, a.uf, x, y, z, cf);
+            const double* xc = X + row * ldx + c;
+            const long long sy = (long long)nx * ldx, sz = sy * ny;
+            const long long offs[7] = {-sz, -sy, -(long long)ldx, 0, (long long)ldx, sy, sz};
+            double v[7][VW];
+#pragma unroll
+            for (int e = 0; e < 7; ++e) {
+#pragma unroll
+                for (int j = 0; j < VW; ++j) v[e][j] = 0.0;
+                if (mk & (1u << e)) {
+                    const double* src = xc + offs[e];
                     if (VW == 1) {
-                        o[0] = __ldcg(src);
+                        v[e][0] = __ldcg(src);
                     } else {
 #pragma unroll
                         for (int h = 0; h < VW / 2; ++h) {
                             const double2 t2 = __ldcg(reinterpret_cast<const double2*>(src) + h);
-                            o[2 * h] = t2.x;
-                            o[(2 * h + 1) % VW] = t2.y;
+                            v[e][2 * h] = t2.x;
+                            v[e][(2 * h + 1) % VW] = t2.y;
                         }
                     }
-                };
-                if (three) {
-                    ld(xc - sz, v[0]);
-                    ld(xc + sz, v[6]);
                 }
-                ld(xc - sy, v[1]);
-                ld(xc - ldx, v[2]);
-                ld(xc, v[3]);
-                ld(xc + ldx, v[4]);
-                ld(xc + sy, v[5]);
-                const double fz = -a.uf.fz, fy = -a.uf.fy, fx = -a.uf.fx, dg = a.uf.dint;
-                double y4[VW];
+            }
+            double p0[VW], acc[VW];
+#pragma unroll
+            for (int j = 0; j < VW; ++j) p0[j] = acc[j] = 0.0;
+            int seen = 0;
+#pragma unroll
+            for (int e = 0; e < 7; ++e) {
+                const bool on = (mk >> e) & 1u;
 #pragma unroll
                 for (int j = 0; j < VW; ++j) {
-                    double p0, acc;
-                    if (three) {
-                        p0 = mul_rn(fz, v[0][j]);
-                        acc = mul_rn(fy, v[1][j]);
-                        acc = add_rn(acc, mul_rn(fx, v[2][j]));
-                    } else {
-                        p0 = mul_rn(fy, v[1][j]);
-                        acc = mul_rn(fx, v[2][j]);
-                    }
-                    acc = add_rn(acc, mul_rn(dg, v[3][j]));
-                    acc = add_rn(acc, mul_rn(fx, v[4][j]));
-                    acc = add_rn(acc, mul_rn(fy, v[5][j]));
-                    if (three) acc = add_rn(acc, mul_rn(fz, v[6][j]));
-                    y4[j] = add_rn(p0, acc);
+                    const double pr = mul_rn(cf[e], v[e][j]);
+                    p0[j] = (on && seen == 0) ? pr : p0[j];
+                    acc[j] = (on && seen == 1) ? pr : ((on && seen > 1) ? add_rn(acc[j], pr) : acc[j]);
                 }
-                double* dst = Y + row * ldy + c;
-                if (VW == 1) {
-                    dst[0] = y4[0];
-                } else {
-#pragma unroll
-                    for (int h = 0; h < VW / 2; ++h)
-                        reinterpret_cast<double2*>(dst)[h] = make_double2(y4[2 * h], y4[(2 * h + 1) % VW]);
-                }
-                continue;
+                seen += on ? 1 : 0;
             }
+            double* dst = Y + row * ldy + c;
+            if (VW == 1) {
+                dst[0] = seen > 1 ? add_rn(p0[0], acc[0]) : p0[0];
+            } else {
+#pragma unroll
+                for (int h = 0; h < VW / 2; ++h)
+                    reinterpret_cast<double2*>(dst)[h] =
+                        make_double2(add_rn(p0[2 * h], acc[2 * h]), add_rn(p0[(2 * h + 1) % VW], acc[(2 * h + 1) % VW]));
+            }
+            continue;
         }
         long long off[8];
         double val[8];
@@ -339,7 +336,7 @@ __device__ __forceinline__ void dmma(double (&acc)[2], double a, double b) {
 // CTA partials exchanged (exchange_sum).
 template <int MT>
 __device__ __forceinline__ void gram_all(Ctx& c, const double* const* X, int d, int ldx, int m1, const double* Y, int ldy, int m2,
-                         long long r0, long long r1, int reg, double* out, double sign = 1.0) {
+                         long long r0, long long r1, int reg, double* out, double sign = 1.0, bool defer = false) {
     constexpr int DMAX = 4 / MT;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, q = lane & 3;
@@ -402,7 +399,7 @@ __device__ __forceinline__ void gram_all(Ctx& c, const double* const* X, int d, 
             for (int w = 0; w + st < kNW; w += 2 * st) pw[w] += pw[w + st];
         exchange_send(c, reg, P, e, pw[0]);
     }
-    exchange_finish(c, reg, P, out, sign);
+    if (!defer) exchange_finish(c, reg, P, out, sign);  // deferred: the caller finishes after independent work
 }
 
 // Fixed-order sum of one value per thread over the CTA, then over the cluster: identical in every CTA.
@@ -779,13 +776,15 @@ __global__ void __launch_bounds__(kNT, 1) cluster_solve_kernel(const Args a) {
         update_local<MT>(nullptr, false, c.one, 1, smem + c.Lp->S, Qnew, m, r0, r1);
         cluster.sync();  // W_k rows visible to the neighbours' operator rows
         PHASE(12);
-        // ---- A W_k, then alpha = W_k^T r (solvers.py:394) ----
-        apply_local<CSR>(a, Qnew, m, AQnew, m, m, r0, r1);
+        // ---- alpha = W_k^T r (solvers.py:394): partials sent now, summed after A W_k (which does not
+        // need alpha), so the exchange is hidden behind the operator rows ----
         if (tid == 0) c.one[0] = Qnew;
         __syncthreads();
-        PHASE(15);
-        gram_all<MT>(c, c.one, 1, m, m, a.r, 1, 1, r0, r1, R_ALPHA, alpha);
+        gram_all<MT>(c, c.one, 1, m, m, a.r, 1, 1, r0, r1, R_ALPHA, alpha, 1.0, true);
         PHASE(13);
+        apply_local<CSR>(a, Qnew, m, AQnew, m, m, r0, r1);
+        exchange_finish(c, R_ALPHA, m, alpha, 1.0);  // ends with a CTA barrier: A W_k rows written
+        PHASE(15);
         // ---- x += W alpha, r -= A W alpha, |r|^2 (solvers.py:395-398) ----
         {
             double part = 0.0;
