@@ -54,3 +54,21 @@ def test_invalid_arguments_rejected_without_launch():
     from paper_2305_19013_b200 import _lib
     with pytest.raises(_lib.KernelError, match="invalid argument"):
         _lib.call("ekcg_split", None, None, None, 10, 0, 0, None, None)
+
+
+def test_cluster_solve_eligibility_and_sass():
+    """The one-kernel cluster solve: which (n, t, window) it covers (a host-only query), and that the
+    kernel really uses distributed shared memory (st.async completing on a peer's mbarrier) and DMMA."""
+    from paper_2305_19013_b200 import _lib
+    fits = lambda n, t, w: _lib.query("ekcg_cluster_solve_fits", n, t, w)  # noqa: E731
+    assert fits(10000, 8, 2) == 1          # BASELINE config 1 (SRE-CG: window 2)
+    assert fits(10000, 8, 4) == 1 and fits(10000, 8, 5) == 0
+    assert fits(4096, 16, 2) == 1 and fits(4096, 16, 3) == 0
+    assert fits(100, 2, 2) == 1 and fits(100, 1, 1) == 1
+    assert fits(10000, 32, 2) == 0         # wide blocks take the launch-per-phase engine
+    assert fits(1 << 22, 8, 2) == 0        # beyond n t = 2^22
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(_lib.library_path())],
+                          capture_output=True, text=True).stdout
+    assert "UCGABAR_ARV" in sass and "UCGABAR_WAIT" in sass  # hardware cluster barrier
+    assert "STAS.64" in sass                                 # st.async into a peer CTA's shared memory
+    assert "SYNCS.ARRIVE.TRANS64" in sass                    # mbarrier expect-tx / complete-tx
