@@ -138,7 +138,7 @@ class DeviceEngine:
         self.nvtx = os.environ.get("EKCG_NVTX", "0") == "1"
         self.use_arena = True  # one allocation for all of a truncated window's blocks (see _setup)
         # whole solve in one thread-block-cluster kernel (csrc/cluster_solve.cu) for small
-        # truncated-window problems: "auto" (n m <= 2^18, where an iteration of separate
+        # truncated-window problems: "auto" (n t up to ~2e5, where an iteration of separate
         # launches is latency-bound), True (whenever the kernel applies) or False
         self.use_cluster = "auto"
         self.cluster_ok = True  # False in the sharded engine
@@ -844,7 +844,10 @@ class DeviceEngine:
         t = self.t_cur
         if not _lib.query("ekcg_cluster_solve_fits", self.n, t, self.window):
             return False
-        if self.use_cluster == "auto" and self.n * t > (1 << 18):
+        # measured crossover against the launch-per-phase engine (tools/cluster_time.py): t = 8 wins up to
+        # n t ~ 2.3e5 (n = 25,600: 88 vs 94 us per iteration; n = 32,761: 106 vs 100), t = 16 (8-CTA
+        # cluster) up to n t ~ 1.3e5
+        if self.use_cluster == "auto" and self.n * t > (200_000 if t <= 8 else 131_072):
             return False
         op = self.op
         if isinstance(op, StencilOperator):
