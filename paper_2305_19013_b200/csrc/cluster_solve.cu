@@ -559,6 +559,85 @@ __device__ __forceinline__ int warp_chol_inverse(double* A, double* R, double* S
     return -1;
 }
 
+// m = 8: the same factor with the matrix held in registers by one warp (lane 4 i + q owns A[i][2 q],
+// A[i][2 q + 1]: the DMMA accumulator layout) and the column steps exchanged by shuffles -- no shared-
+// memory round trips inside the column loop.  PRE: Pre-CholQR (column norms D from the raw diagonal, the
+// factor of sym(D^-1 G D^-1), output D^-1 R^-1); else the plain factor of sym(G), output R^-1.
+// Called by one whole warp; returns 0 ok / 1 zero column / 2 pivot breakdown.
+template <bool PRE>
+__device__ __forceinline__ int warp_factor8(const double* G, double* Rs, double* Sout, double* rinv, double* inrm,
+                                            double tol, int& col, double& piv_out, double& scale_out) {
+    const int lane = threadIdx.x & 31, i = lane >> 2, q = lane & 3, k0 = 2 * q;
+    double a0 = 0.5 * (G[i * 8 + k0] + G[k0 * 8 + i]);
+    double a1 = 0.5 * (G[i * 8 + k0 + 1] + G[(k0 + 1) * 8 + i]);
+    if (PRE) {
+        const int j = lane & 7;
+        const double dg = G[j * 8 + j];
+        const unsigned zero = __ballot_sync(0xffffffffu, lane < 8 && dg == 0.0);
+        if (zero) {
+            col = __ffs((int)zero) - 1;
+            piv_out = 0.0;
+            scale_out = 0.0;
+            return 1;
+        }
+        const double ir = rsqrt(dg);  // NaN for a negative / NaN diagonal: the first pivot test then fails
+        if (lane < 8) inrm[lane] = ir;
+        const double ii = __shfl_sync(0xffffffffu, ir, i);
+        const double ik0 = __shfl_sync(0xffffffffu, ir, k0);
+        const double ik1 = __shfl_sync(0xffffffffu, ir, k0 + 1);
+        a0 *= ii * ik0;
+        a1 *= ii * ik1;
+    }
+    double sc = (k0 == i) ? fabs(a0) : ((k0 + 1 == i) ? fabs(a1) : 0.0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sc = fmax(sc, __shfl_xor_sync(0xffffffffu, sc, o));
+    scale_out = sc;
+    double r0 = 0.0, r1 = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const double piv = __shfl_sync(0xffffffffu, (j & 1) ? a1 : a0, 4 * j + (j >> 1));
+        if (!isfinite(piv) || piv <= tol * sc) {
+            col = j;
+            piv_out = piv;
+            return 2;
+        }
+        const double ri = rsqrt(piv);
+        const double rjj = piv * ri;
+        const double ajk0 = __shfl_sync(0xffffffffu, a0, 4 * j + q);  // A[j][2 q], A[j][2 q + 1]
+        const double ajk1 = __shfl_sync(0xffffffffu, a1, 4 * j + q);
+        const double t0 = __shfl_sync(0xffffffffu, a0, 4 * j + (i >> 1));  // A[j][i]
+        const double t1 = __shfl_sync(0xffffffffu, a1, 4 * j + (i >> 1));
+        const double rji = ((i & 1) ? t1 : t0) * ri;
+        if (i == j) {
+            r0 = k0 > j ? a0 * ri : (k0 == j ? rjj : 0.0);
+            r1 = k0 + 1 > j ? a1 * ri : (k0 + 1 == j ? rjj : 0.0);
+        }
+        if (i > j) {
+            a0 -= rji * (ajk0 * ri);
+            a1 -= rji * (ajk1 * ri);
+        }
+        if (lane == 0) rinv[j] = ri;
+    }
+    Rs[i * 8 + k0] = r0;
+    Rs[i * 8 + k0 + 1] = r1;
+    __syncwarp();
+    if (lane < 8) {
+        const int cc = lane;
+        double colv[8];
+#pragma unroll
+        for (int r = 7; r >= 0; --r) {
+            double acc = 0.0;
+#pragma unroll
+            for (int k = r + 1; k < 8; ++k) acc += (k <= cc) ? Rs[r * 8 + k] * colv[k] : 0.0;
+            colv[r] = (r > cc) ? 0.0 : (r == cc) ? rinv[cc] : -acc * rinv[r];
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) Sout[r * 8 + cc] = PRE ? colv[r] * inrm[r] : colv[r];
+    }
+    __syncwarp();
+    return 0;
+}
+
 // Pre-CholQR factor S0 = D^-1 chol(sym(D^-1 G D^-1))^-1 (aortho.py:74-79, 104-106) from G = W^T W.
 // 0 ok, 1 zero column, 2 pivot breakdown (col / piv / scale describe it).
 template <int MB>
@@ -570,7 +649,19 @@ __device__ __forceinline__ int prechol_local(Ctx& c, int m, double tol, int& col
     double* R = c.sm + c.Lp->R;
     double* S = c.sm + c.Lp->S;
     double* S0 = c.sm + c.Lp->S0;
-    if (threadIdx.x < 32) {
+    if (MB == 8 && m == 8) {
+        if (threadIdx.x < 32) {
+            int bad = -1;
+            double pv = 0.0, scv = 0.0;
+            const int kind = warp_factor8<true>(G, R, S0, rinv, inrm, tol, bad, pv, scv);
+            if (threadIdx.x == 0) {
+                res[0] = kind;
+                res[1] = bad;
+                resd[0] = pv;
+                resd[1] = scv;
+            }
+        }
+    } else if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         int kind = 0, bad = -1;
         double pv = 0.0, scv = 0.0;
@@ -628,7 +719,20 @@ __device__ __forceinline__ int cholinv_local(Ctx& c, int m, double tol, int& col
     double* G = c.sm + c.Lp->G;
     double* R = c.sm + c.Lp->R;
     double* S = c.sm + c.Lp->S;
-    if (threadIdx.x < 32) {
+    if (MB == 8 && m == 8) {
+        if (threadIdx.x < 32) {
+            __shared__ double unused_inrm[8];
+            int bad = -1;
+            double pv = 0.0, scv = 0.0;
+            const int kind = warp_factor8<false>(G, R, S, rinv, unused_inrm, tol, bad, pv, scv);
+            if (threadIdx.x == 0) {
+                res[0] = kind;
+                res[1] = bad;
+                resd[0] = pv;
+                resd[1] = scv;
+            }
+        }
+    } else if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         double pv = 0.0, scv = 0.0;
         for (int e = lane; e < m * m; e += 32) {
