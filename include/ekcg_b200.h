@@ -250,8 +250,9 @@ int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx, double* Y
  * thread-block cluster (up to 16 CTAs, distributed-shared-memory reductions,
  * hardware cluster barriers): for problems whose blocks live in L2, where an
  * iteration of separate launches is latency-bound.  Unpreconditioned, s = 1,
- * t <= 16, window * t^2 <= 512; the operator is the stencil `desc` (whole
- * grid) or, with desc == NULL, a CSR matrix whose rows hold at most 8 entries.
+ * t <= 16, window <= 4 (t <= 8) or <= 2 (t <= 16), n t <= 2^22
+ * (ekcg_cluster_solve_fits); the operator is the stencil `desc` (whole grid)
+ * or, with desc == NULL, a CSR matrix whose rows hold at most 8 entries.
  * Before the call: x = x0, r = b - A x0, and ctrl / history[0] initialised by
  * ekcg_start.  `blocks` is scratch of (2 window + 3) * span + n doubles (span >=
  * n t, a multiple of 32).  On return (stream order) ctrl holds the final

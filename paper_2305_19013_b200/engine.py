@@ -832,7 +832,7 @@ class DeviceEngine:
     # -------------------------------------------------------- cluster solve
     def _cluster_eligible(self):
         """The one-kernel cluster solve (csrc/cluster_solve.cu) covers unpreconditioned SRE-CG /
-        SRE-CG2 with a truncation window, s = 1, t <= 16, window t^2 <= 512, on a whole-grid
+        SRE-CG2 with a truncation window, s = 1, t <= 16, window <= 4 (t <= 8) or 2 (t = 16), on a whole-grid
         stencil operator or a CSR matrix with rows of at most 8 entries."""
         from .operators import CsrOperator, StencilOperator
         if not self.cluster_ok or self.use_cluster is False or self.kernel_timer is not None or self.no_fuse:

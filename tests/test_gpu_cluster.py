@@ -157,3 +157,41 @@ def test_cluster_not_taken_when_ineligible():
     eng = DeviceEngine(prob.stencil(), prob.partition, SolverConfig(**dict(prob.solver_kwargs, kmax=5)))
     eng.solve(prob.b)
     assert not eng.ran_cluster
+
+
+@pytest.mark.parametrize("t,shape,window", [(1, (30, 30), 2), (3, (30, 30), 3), (5, (24, 20), 2), (7, (31, 17), 4),
+                                            (12, (20, 20), 2), (2, (10, 10), 2), (6, (9, 8, 7), 2)])
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+def test_cluster_any_width_and_ragged_rows(t, shape, window, form):
+    """Odd and non-power-of-two block widths (scalar load / store paths, runtime-width DMMA tiles), grids
+    whose row count is no multiple of the 8-row tiles, and problems with fewer rows than the cluster has
+    row slots (some CTAs own no rows)."""
+    from paper_2305_19013_b200.partition import Partition
+    rng = np.random.default_rng(100 + t)
+    n = int(np.prod(shape))
+    op = pk.StencilOperator(shape, kappa=1.0 + 0.25 * t)
+    A = op if form == "stencil" else op.to_csr()
+    owner = (np.arange(n) * t // n).astype(np.int64)
+    part = Partition.from_owner(owner, t)
+    b = rng.uniform(-1.0, 1.0, n)
+    cfg = SolverConfig(method="sre-cg2", t=t, tol=1e-9, retention="trunc", trunc=window, true_residual_every=5)
+    (xa, a), (xb, b_) = _engines(A, part, cfg, b)
+    assert a.status == b_.status == "converged"
+    assert abs(a.iterations - b_.iterations) <= max(1, round(0.02 * b_.iterations))
+    assert hist_dev(a.residual_history, b_.residual_history) <= 1e-9
+    assert a.peak_block_vectors == b_.peak_block_vectors or a.iterations != b_.iterations
+    assert len(a.true_residual_checks) == a.iterations // 5
+    assert np.linalg.norm(xa - xb) <= 1e-7 * np.linalg.norm(xb)
+    assert a.true_residual <= 1e-8 * np.linalg.norm(b)
+
+
+def test_cluster_zero_rhs_and_exact_start():
+    """rho0 = 0: converged with no iteration (solvers.py:343-345); a start at the solution likewise stops at once."""
+    prob = make_config(1, 40)
+    cfg = SolverConfig(**prob.solver_kwargs)
+    eng = DeviceEngine(prob.stencil(), prob.partition, cfg)
+    x, rep = eng.solve(np.zeros(prob.n))
+    assert eng.ran_cluster and rep.status == "converged" and rep.iterations == 0 and not np.any(x)
+    eng = DeviceEngine(prob.stencil(), prob.partition, SolverConfig(**dict(prob.solver_kwargs, kmax=1)))
+    x, rep = eng.solve(prob.b)
+    assert eng.ran_cluster and rep.status == "maxiter" and rep.iterations == 1 and len(rep.residual_history) == 2
