@@ -11,6 +11,20 @@ ROOT = Path(__file__).resolve().parent.parent
 HEADER = ROOT / "include" / "ekcg_b200.h"
 
 
+_SASS = {}
+
+
+def library_sass():
+    """cuobjdump -sass of the library, dumped once per test session (the dump takes ~20 s)."""
+    from paper_2305_19013_b200 import _lib
+    path = _lib.library_path()
+    _lib.load()
+    if "sass" not in _SASS:
+        _SASS["sass"] = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(path)], capture_output=True,
+                                       text=True).stdout
+    return _SASS["sass"]
+
+
 def declared_functions():
     text = HEADER.read_text()
     text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
@@ -37,9 +51,7 @@ def test_library_is_sm100a():
     out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(path)], capture_output=True,
                          text=True)
     assert "sm_100a" in out.stdout
-    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(path)], capture_output=True,
-                          text=True).stdout
-    assert "DMMA.8x8x4" in sass  # fp64 tensor-core Gram/update kernels
+    assert "DMMA.8x8x4" in library_sass()  # fp64 tensor-core Gram/update kernels
 
 
 def test_host_only_queries_without_gpu():
@@ -67,8 +79,7 @@ def test_cluster_solve_eligibility_and_sass():
     assert fits(100, 2, 2) == 1 and fits(100, 1, 1) == 1
     assert fits(10000, 32, 2) == 0         # wide blocks take the launch-per-phase engine
     assert fits(1 << 22, 8, 2) == 0        # beyond n t = 2^22
-    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", str(_lib.library_path())],
-                          capture_output=True, text=True).stdout
+    sass = library_sass()
     assert "UCGABAR_ARV" in sass and "UCGABAR_WAIT" in sass  # hardware cluster barrier
     assert "STAS.64" in sass                                 # st.async into a peer CTA's shared memory
     assert "SYNCS.ARRIVE.TRANS64" in sass                    # mbarrier expect-tx / complete-tx
