@@ -267,6 +267,16 @@ int ekcg_cluster_solve(const EkcgStencil* desc, const long long* row_ptr, const 
                        long long span, void* ctrl, double* history, double* checks, double chol_tol,
                        long long* phase_ticks, void* stream);
 
+/* Classical unpreconditioned CG (`cg`, solvers.py:199-258) as one kernel on one thread-block
+ * cluster, for small problems (n <= 2^22; rows of at most 8 entries in CSR form): one cluster
+ * barrier and two scalar exchanges per iteration, no host reads inside the loop.  Before the
+ * call: x = x0, r = b - A x0, ctrl / history[0] initialised by ekcg_start (tol_abs = tol * rho0).
+ * `scratch` holds 2 n doubles (p, A p).  On return ctrl holds status (1 converged, 2 maxiter,
+ * 3 = nonpositive curvature with brk_pivot = p^T A p and brk_iter = the iteration) and k_done. */
+int ekcg_cluster_cg(const EkcgStencil* desc, const long long* row_ptr, const int* col_idx,
+                    const double* values, long long n, int kmax, double* x, double* r, double* scratch,
+                    void* ctrl, double* history, void* stream);
+
 /* ---- engine bookkeeping ------------------------------------------------ */
 
 /* Size in bytes of the control block. */

@@ -1025,6 +1025,154 @@ int launch_cluster_m(const Args& a, cudaStream_t st) {
     return a.t < 8 ? launch_cluster<CSR, 1, 0>(a, st) : launch_cluster<CSR, 2, 0>(a, st);
 }
 
+
+// ---------------------------------------------------------------------------
+// Classical CG (solvers.py:199-258, unpreconditioned: z = r) on the same cluster machinery: one cluster
+// barrier (p visible to the neighbours' operator rows) and two scalar exchanges (p^T A p, |r|^2) per
+// iteration.  The launch-per-phase `cg` reads three scalars back to the host every iteration.
+// ---------------------------------------------------------------------------
+struct CgArgs {
+    Args op;        // operator, n, kmax, x, r, ctrl, history (t = window = 1)
+    double* p;      // n
+    double* ap;     // n
+};
+
+template <bool CSR>
+__global__ void __launch_bounds__(kNT, 1) cluster_cg_kernel(const CgArgs ca) {
+    extern __shared__ __align__(16) double smem[];
+    const Args& a = ca.op;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int tid = threadIdx.x;
+    const long long n = a.n;
+    __shared__ Layout s_layout;
+    if (tid == 0) s_layout = make_layout(1, 1, (int)cluster.num_blocks());
+    __syncthreads();
+    Ctx c;
+    c.sm = smem;
+    c.Lp = &s_layout;
+    c.bar = reinterpret_cast<unsigned long long*>(smem + c.Lp->misc);
+    c.qp = c.aqp = c.one = nullptr;
+    c.rank = cluster.block_rank();
+    c.cl = cluster.num_blocks();
+    c.parity = 0;
+    const long long per = (n + c.cl - 1) / c.cl;
+    const long long r0 = min(n, (long long)c.rank * per), r1 = min(n, r0 + per);
+    const bool lead = (c.rank == 0 && tid == 0);
+    if (tid == 0) {
+        for (int i = 0; i < R_COUNT; ++i) mbar_init(c.bar + i, 1);
+        mbar_fence_init();
+    }
+    cluster.sync();
+
+    pdl_wait();
+    EkcgCtrl* ctrl = a.ctrl;
+    const bool run = ctrl->live != 0;  // rho0 == 0: converged before the first iteration
+    const double tol_abs = ctrl->tol_abs;
+    double* __restrict__ p = ca.p;
+    double* __restrict__ ap = ca.ap;
+    double rz = 0.0, rho = ctrl->last_rho, pAp = 0.0;
+    int status = 0, k = 1;
+    if (run) {
+        double part = 0.0;
+        for (long long row = r0 + tid; row < r1; row += kNT) {
+            const double rv = a.r[row];
+            p[row] = rv;  // p = z = r
+            part = fma(rv, rv, part);
+        }
+        rz = scalar_all(c, part, R_CHECK);  // r . z
+    }
+    for (; run; ++k) {
+        cluster.sync();  // every CTA's p rows written
+        apply_local<CSR>(a, p, 1, ap, 1, 1, r0, r1);
+        __syncthreads();
+        double part = 0.0;
+        for (long long row = r0 + tid; row < r1; row += kNT) part = fma(p[row], ap[row], part);
+        pAp = scalar_all(c, part, R_CHECK);  // (two-slot scalar regions: R_CHECK, R_RHO)
+        if (pAp <= 0.0) {  // nonpositive curvature (solvers.py:228-231)
+            status = 3;
+            break;
+        }
+        const double alpha = rz / pAp;
+        part = 0.0;
+        for (long long row = r0 + tid; row < r1; row += kNT) {
+            a.x[row] = fma(alpha, p[row], a.x[row]);
+            const double rn = fma(-alpha, ap[row], a.r[row]);
+            a.r[row] = rn;
+            part = fma(rn, rn, part);
+        }
+        const double rz_new = scalar_all(c, part, R_RHO);
+        rho = sqrt(rz_new);
+        if (lead) a.history[k] = rho;
+        if (rho <= tol_abs) {
+            status = 1;
+            break;
+        }
+        if (!(rho > tol_abs) || k + 1 > a.kmax) {
+            status = 2;
+            break;
+        }
+        const double beta = rz_new / rz;
+        rz = rz_new;
+        for (long long row = r0 + tid; row < r1; row += kNT) p[row] = fma(beta, p[row], a.r[row]);
+    }
+    if (lead && run) {
+        if (status == 3) {
+            ctrl->brk_kind = 3;
+            ctrl->brk_pivot = pAp;
+            ctrl->brk_iter = k;
+            ctrl->k_done = k - 1;
+        } else {
+            ctrl->k_done = k;
+            ctrl->last_rho = rho;
+        }
+        ctrl->status = status;
+        ctrl->live = 0;
+    }
+    cluster.sync();
+}
+
+template <bool CSR>
+int launch_cluster_cg(const CgArgs& ca, cudaStream_t st) {
+    auto fn = cluster_cg_kernel<CSR>;
+    static bool ready[kEkcgMaxDevices];
+    const int dev = ekcg_device();
+    if (!ready[dev]) {
+        if (cudaFuncSetAttribute((const void*)fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+            cudaGetLastError();
+            return EKCG_ELAUNCH;
+        }
+        ready[dev] = true;
+    }
+    for (int cl = kMaxCl; cl >= 1; cl >>= 1) {
+        const size_t smem = sizeof(double) * (size_t)make_layout(1, 1, cl).total;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(cl);
+        cfg.blockDim = dim3(kNT);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = st;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = cl;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        int clusters = 0;
+        if (cudaOccupancyMaxActiveClusters(&clusters, (const void*)fn, &cfg) != cudaSuccess || clusters < 1) {
+            cudaGetLastError();
+            continue;
+        }
+        if (cudaLaunchKernelEx(&cfg, fn, ca) == cudaSuccess) {
+            ++g_ekcg_launches;
+            return EKCG_OK;
+        }
+        cudaGetLastError();
+    }
+    return EKCG_ELAUNCH;
+}
+
 }  // namespace
 
 extern "C" int ekcg_cluster_solve_fits(long long n, int t, int window) {
@@ -1071,4 +1219,36 @@ extern "C" int ekcg_cluster_solve(const EkcgStencil* desc, const long long* row_
     a.ci = col_idx;
     a.vv = values;
     return launch_cluster_m<true>(a, as_stream(stream));
+}
+
+extern "C" int ekcg_cluster_cg(const EkcgStencil* desc, const long long* row_ptr, const int* col_idx,
+                               const double* values, long long n, int kmax, double* x, double* r, double* scratch,
+                               void* ctrl, double* history, void* stream) {
+    if (n < 1 || n > (1LL << 22) || kmax < 1) return EKCG_EINVAL;
+    if (x == nullptr || r == nullptr || scratch == nullptr || ctrl == nullptr || history == nullptr)
+        return EKCG_EINVAL;
+    CgArgs ca = {};
+    Args& a = ca.op;
+    a.n = n;
+    a.t = 1;
+    a.window = 1;
+    a.kmax = kmax;
+    a.every = 1;
+    a.x = x;
+    a.r = r;
+    a.ctrl = (EkcgCtrl*)ctrl;
+    a.history = history;
+    ca.p = scratch;
+    ca.ap = scratch + n;
+    if (desc != nullptr) {
+        long long ns = 0;
+        if (prepare_stencil(desc, a.s, a.uf, ns) != EKCG_OK || ns != n) return EKCG_EINVAL;
+        if (a.s.row_begin != 0 || a.s.row_end != n) return EKCG_EINVAL;
+        return launch_cluster_cg<false>(ca, as_stream(stream));
+    }
+    if (row_ptr == nullptr || col_idx == nullptr || values == nullptr) return EKCG_EINVAL;
+    a.rp = row_ptr;
+    a.ci = col_idx;
+    a.vv = values;
+    return launch_cluster_cg<true>(ca, as_stream(stream));
 }

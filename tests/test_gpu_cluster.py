@@ -195,3 +195,49 @@ def test_cluster_zero_rhs_and_exact_start():
     eng = DeviceEngine(prob.stencil(), prob.partition, SolverConfig(**dict(prob.solver_kwargs, kmax=1)))
     x, rep = eng.solve(prob.b)
     assert eng.ran_cluster and rep.status == "maxiter" and rep.iterations == 1 and len(rep.residual_history) == 2
+
+
+@pytest.mark.parametrize("shape,form", [((100, 100), "stencil"), ((100, 100), "csr"), ((17, 13, 11), "stencil"),
+                                        ((9, 7), "csr")])
+def test_cluster_cg_matches_launch_per_phase_cg(shape, form, monkeypatch):
+    """Classical CG (solvers.py:199-258) as one cluster kernel (ekcg_cluster_cg) against the launch-per-phase
+    loop on the same inputs: same status and iteration count, history to round-off."""
+    import importlib
+    cg_mod = importlib.import_module("paper_2305_19013_b200.cg")
+    rng = np.random.default_rng(5)
+    op = pk.StencilOperator(shape, kappa=1.5)
+    A = op if form == "stencil" else op.to_csr()
+    n = int(np.prod(shape))
+    x_star = rng.standard_normal(n)
+    b = pk.spmv(op.to_csr(), x_star)
+    cfg = SolverConfig(method="cg", tol=1e-9)
+    reps = []
+    for cap in (1 << 18, 0):
+        monkeypatch.setattr(cg_mod, "CLUSTER_CG_MAX_N", cap)
+        launches0 = cg_mod._lib.query("ekcg_launch_count")
+        x, rep = pk.cg(A, b, cfg=cfg, x_star=x_star)
+        reps.append((x, rep, cg_mod._lib.query("ekcg_launch_count") - launches0))
+    (xa, a, la), (xb, b_, lb) = reps
+    assert la < 20 < lb, "the first run should be one cluster kernel, the second one launch per phase"
+    assert a.status == b_.status == "converged"
+    assert abs(a.iterations - b_.iterations) <= max(1, round(0.02 * b_.iterations))
+    assert hist_dev(a.residual_history, b_.residual_history) <= 1e-9
+    assert a.relative_error < 1e-6 and np.linalg.norm(xa - xb) <= 1e-7 * np.linalg.norm(xb)
+
+
+def test_cluster_cg_breakdown_and_kmax(monkeypatch):
+    """Nonpositive curvature stops with the reference's status and note; kmax reports maxiter."""
+    n = 64
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int64)
+    vals = np.ones(n)
+    vals[3] = -2.0  # indefinite diagonal matrix
+    A = pk.SparseSpdMatrix(n, rp, ci, vals, validate=False)
+    b = np.zeros(n)
+    b[3] = 1.0
+    x, rep = pk.cg(A, b, cfg=SolverConfig(method="cg"))
+    assert rep.status == "breakdown" and rep.iterations == 0
+    assert rep.notes == ["nonpositive curvature p^T A p = -2.000e+00 at iteration 1"]
+    prob = make_config(1, 40)
+    x, rep = pk.cg(prob.stencil(), prob.b, cfg=SolverConfig(method="cg", kmax=7))
+    assert rep.status == "maxiter" and rep.iterations == 7 and len(rep.residual_history) == 8
