@@ -219,6 +219,8 @@ class DeviceEngine:
             return True
         block = 8.0 * n * m
         cached = (2 * self.window + 3) * block + 6 * 8.0 * n
+        if cached < (1 << 30):  # small solves: no cudaMemGetInfo round trip (~0.2 ms of a 6 ms config-1 call)
+            return False
         free, _ = torch.cuda.mem_get_info(self.device)
         return cached > 0.92 * free
 
