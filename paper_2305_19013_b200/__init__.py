@@ -19,7 +19,7 @@ from .linalg import (
 from .partition import Partition, contiguous_partition, read_partition, write_partition
 from .aortho import a_cholqr, a_orthogonalize_against, pre_cholqr
 from .cg import cg
-from .operators import CsrOperator, StencilOperator
+from .operators import CsrOperator, StencilOperator, as_operator
 from .solvers import (
     METHODS,
     RETENTIONS,
@@ -67,6 +67,7 @@ __all__ = [
     "a_cholqr",
     "pre_cholqr",
     "CsrOperator",
+    "as_operator",
     "StencilOperator",
     "METHODS",
     "RETENTIONS",

@@ -16,6 +16,9 @@ from . import _lib
 from .device import current_stream_ptr, get_device
 
 
+EKCG_COEF_STRIDE = {2: 6, 3: 8}
+
+
 def _ptr(x):
     return x if isinstance(x, int) else x.data_ptr()
 
@@ -149,14 +152,102 @@ class StencilOperator:
                       current_stream_ptr(self.device))
             desc.coef = self.coef.data_ptr()
 
+    @classmethod
+    def from_csr(cls, csr):
+        """The grid-stencil form of a CSR matrix whose sparsity pattern is exactly the 5- / 7-point
+        pattern of an nx x ny (x nz) grid in x-fastest order (what `_diffusion_matrix`,
+        `gen_poisson2d/3d` and any finite-volume assembly on a box grid produce), or None.
+
+        The values go, unchanged, into the per-node coefficient table the plane-march and fused
+        stencil kernels already read (EkcgStencil.coef: slot order z-, y-, x-, diag, x+, y+, z+), so
+        every product is bitwise the CSR product (same entries, same order, same association) while
+        each X row is staged once through shared memory instead of gathered up to 7 times from L2,
+        and the fused m <= 16 kernels and the matrix-free cluster path apply.  The check is exact:
+        row pointers and every column index must equal the grid pattern's (done on the device)."""
+        n = int(csr.n)
+        rp, ci, vals = csr.row_ptr, csr.col_idx, csr.values
+        if n < 4 or rp.numel() != n + 1:
+            return None
+        dev = rp.device
+        head = rp[:2].cpu().tolist()
+        cnt0 = head[1] - head[0]
+        if head[0] != 0 or cnt0 not in (3, 4):
+            return None
+        c0 = ci[:cnt0].cpu().tolist()
+        if c0[0] != 0 or c0[1] != 1 or c0[2] < 2:
+            return None
+        nx = int(c0[2])
+        if cnt0 == 4:
+            nxy = int(c0[3])
+            if nxy % nx or n % nxy:
+                return None
+            ny, nz, dim = nxy // nx, n // nxy, 3
+        else:
+            if n % nx:
+                return None
+            ny, nz, dim, nxy = n // nx, 1, 2, n
+        if ny < 2 or (dim == 3 and nz < 2) or n >= (1 << 31):
+            return None
+        i = torch.arange(n, dtype=torch.int64, device=dev)
+        x, y, z = i % nx, (i // nx) % ny, i // nxy
+        true = torch.ones(n, dtype=torch.bool, device=dev)
+        slots = [(-nxy, z > 0), (-nx, y > 0), (-1, x > 0), (0, true), (1, x < nx - 1), (nx, y < ny - 1),
+                 (nxy, z < nz - 1)]
+        if dim == 2:
+            slots = slots[1:6]
+        count = torch.zeros(n, dtype=torch.int64, device=dev)
+        for _, present in slots:
+            count += present
+        expect_rp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+        torch.cumsum(count, 0, out=expect_rp[1:])
+        nnz = int(ci.numel())
+        # one verdict, read back once: row pointers equal, and every present slot holds the grid neighbour
+        ok = (expect_rp == rp.to(torch.int64)).all() & (expect_rp[-1] == nnz)
+        stride = 8 if dim == 3 else 6
+        table = torch.zeros(n, stride, dtype=torch.float64, device=dev)
+        pos = expect_rp[:-1].clone()
+        last = max(nnz - 1, 0)
+        for slot, (off, present) in enumerate(slots):
+            at = pos.clamp(max=last)
+            ok = ok & torch.where(present, ci[at].to(torch.int64) == i + off, true).all()
+            table[:, slot] = torch.where(present, vals[at], table[:, slot])
+            pos += present
+        if not bool(ok):
+            return None
+        op = cls.__new__(cls)
+        op.device = dev
+        op.shape = (nx, ny) if dim == 2 else (nx, ny, nz)
+        op.dim, op.n = dim, n
+        op.axis_coef = (1.0,) * dim
+        op.field = op.field_host = None
+        op.coef = table.reshape(-1)
+        op.tile = (1, 1, 1)
+        op.nnz = int(ci.numel())
+        op.host = getattr(csr, "host", None)
+        op.from_matrix = True
+        desc = _lib.EkcgStencil()
+        desc.dim, desc.nx, desc.ny, desc.nz = dim, nx, ny, nz
+        desc.cx = desc.cy = desc.cz = 1.0
+        desc.kfield = op.coef.data_ptr()  # non-null marks a variable-coefficient operator; never read:
+        desc.coef = op.coef.data_ptr()    # every kernel takes a node's row from the table
+        desc.tx = desc.ty = desc.tz = 1
+        desc.fx, desc.fy = nx, ny
+        desc.kconst = 0.0
+        op._desc = desc
+        return op
+
     def matrix_bytes(self):
         """M_A of the SURVEY 8(d) traffic model: 0 for constant kappa, 8 n (a node-kappa array) for a
         kappa field.  The kernels actually stream the per-node coefficient table (48 n / 64 n bytes
         in 2-D / 3-D); DESIGN.md section 3 and the ncu traffic columns account for it."""
+        if getattr(self, "from_matrix", False):  # the coefficient table of a CSR matrix in grid form
+            return 8 * EKCG_COEF_STRIDE[self.dim] * self.n
         return 0 if self.field is None else 8 * self.n
 
     def node_kappa(self):
         """Full node-kappa array (host), x fastest."""
+        if getattr(self, "from_matrix", False):
+            raise ValueError("an operator built from a CSR matrix has no kappa field")
         if self.field_host is None:
             return np.full(self.n, self._desc.kconst)
         f = self.field_host
@@ -178,11 +269,37 @@ class StencilOperator:
         _lib.call("ekcg_spmm_stencil", ctypes.byref(self._desc), _ptr(X), ldx, _ptr(Y), ldy, m, live, st)
 
 
+# CSR matrices with an exact grid-stencil pattern are applied in stencil form (StencilOperator.from_csr):
+# bitwise the same products, stencil-kernel speed.  False keeps every CSR matrix on the CSR kernels.
+DETECT_GRID = True
+
+
 def as_operator(A, device=None):
     if isinstance(A, (CsrOperator, StencilOperator, HatOperator)):
         return A
     if hasattr(A, "row_ptr") and hasattr(A, "col_idx") and hasattr(A, "values"):
-        return CsrOperator(A, device)
+        dev = get_device(device)
+        # the operator is cached on the host matrix (immutable by contract: SparseSpdMatrix keeps its
+        # device arrays in `_dev` the same way)
+        cache = getattr(A, "_dev", None)
+        if not isinstance(cache, dict):
+            cache = getattr(A, "_ekcg_ops", None)
+            if cache is None:
+                cache = {}
+                try:
+                    setattr(A, "_ekcg_ops", cache)
+                except AttributeError:
+                    pass
+        key = ("operator", str(dev), bool(DETECT_GRID))
+        if key in cache:
+            return cache[key]
+        op = CsrOperator(A, dev)
+        if DETECT_GRID:
+            grid = StencilOperator.from_csr(op)
+            if grid is not None:
+                op = grid
+        cache[key] = op
+        return op
     raise TypeError(f"unsupported operator type {type(A).__name__}")
 
 

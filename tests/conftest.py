@@ -15,6 +15,7 @@ sys.path.insert(0, str(ROOT))
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200)")
     config.addinivalue_line("markers", "slow: long-running parity case")
+    config.addinivalue_line("markers", "grid_detect: run with CSR grid-pattern detection on (the product default)")
 
 
 def _cuda_available():
@@ -61,3 +62,17 @@ def golden_case_inputs(arrays, name):
     """(row_ptr, col_idx, values, b, owner, x0) stored for a small golden case."""
     g = lambda k: arrays.get(f"{name}__{k}")
     return g("rp"), g("ci"), g("vals"), g("b"), g("owner"), g("x0")
+
+
+@pytest.fixture(autouse=True)
+def _csr_matrices_stay_csr(request, monkeypatch):
+    """The product applies CSR matrices with an exact grid-stencil pattern in stencil form
+    (operators.DETECT_GRID).  The suite keeps them on the CSR kernels, so that the CSR paths stay covered;
+    tests marked `grid_detect` (tests/test_gpu_grid_detect.py) run with the product default."""
+    if "grid_detect" in request.keywords:
+        yield
+        return
+    from paper_2305_19013_b200 import operators
+    monkeypatch.setattr(operators, "DETECT_GRID", False)
+    yield
+
