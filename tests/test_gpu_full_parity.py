@@ -87,6 +87,24 @@ def test_cfg3_full_size_vs_real_reference_csr_form():
     assert rep.iterations == fx["iterations"] and dev.max() <= HIST_TOL, dev
 
 
+@pytest.mark.grid_detect
+def test_cfg3_full_size_vs_real_reference_csr_form_grid_detected():
+    """The product default for the same host CSR matrix: its 7-point grid pattern is detected and the
+    matrix applied in stencil form from a table of its own values (bitwise the CSR products)."""
+    from paper_2305_19013_b200.engine import DeviceEngine
+    from paper_2305_19013_b200.operators import StencilOperator
+    fx = _fixture("cfg3")
+    prob = make_config(3, fx["edge"])
+    A = prob.csr()
+    kw = dict(prob.solver_kwargs, kmax=fx["k"])
+    eng = DeviceEngine(A, prob.partition, pk.SolverConfig(**kw))
+    assert isinstance(eng.op, StencilOperator) and eng.op.from_matrix
+    x, rep = eng.solve(prob.b)
+    h, g = np.asarray(rep.residual_history), np.asarray(fx["residual_history"])
+    dev = np.abs(h / h[0] - g / g[0]) / (g / g[0])
+    assert rep.iterations == fx["iterations"] and dev.max() <= HIST_TOL, dev
+
+
 def test_cfg4_full_size_vs_oracle():
     fx = _fixture("cfg4")
     _run(4, fx)
