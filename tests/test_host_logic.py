@@ -125,3 +125,55 @@ class TestPeakReplay:
         e = self._engine(None, restarts=[6])
         e.launch_k = [(k, 0, 2) for k in range(1, 11)]
         assert e._replay_peak(10) == 10
+
+
+def test_grid_pattern_detection_on_cpu_tensors():
+    """StencilOperator.from_csr (operators.py) is plain tensor arithmetic: exact 5- / 7-point grid patterns
+    give a coefficient table holding the matrix's own values in slot order; anything else gives None."""
+    import types
+
+    import numpy as np
+    import torch
+
+    from paper_2305_19013_b200.operators import StencilOperator
+    from paper_2305_19013_b200.problems import diffusion_csr
+
+    def fake(A):
+        return types.SimpleNamespace(n=A.n, row_ptr=torch.from_numpy(np.asarray(A.row_ptr, dtype=np.int64)),
+                                     col_idx=torch.from_numpy(np.asarray(A.col_idx).astype(np.int32)),
+                                     values=torch.from_numpy(np.asarray(A.values, dtype=np.float64)), host=A)
+
+    rng = np.random.default_rng(1)
+    for shape in ((5, 4), (3, 4, 5), (2, 2), (2, 2, 2), (7, 3, 2)):
+        n = int(np.prod(shape))
+        A = diffusion_csr(shape, np.exp(rng.uniform(-1, 1, n)))
+        op = StencilOperator.from_csr(fake(A))
+        assert op is not None and op.shape == shape and op.n == n and op.nnz == A.nnz
+        dim = len(shape)
+        stride = 8 if dim == 3 else 6
+        table = op.coef.reshape(n, stride).numpy()
+        dense = A.to_dense()
+        nx = shape[0]
+        nxy = shape[0] * shape[1]
+        offs = [-nxy, -nx, -1, 0, 1, nx, nxy] if dim == 3 else [-nx, -1, 0, 1, nx]
+        for i in range(n):
+            for slot, off in enumerate(offs):
+                j = i + off
+                want = dense[i, j] if 0 <= j < n and dense[i, j] != 0.0 else 0.0
+                # x neighbours do not wrap across grid lines: the pattern has no entry there
+                assert table[i, slot] == want, (shape, i, slot)
+        assert np.all(table[:, len(offs):] == 0.0)
+    # not a grid: an entry moved, a permuted matrix, a 1-D chain
+    A = diffusion_csr((4, 4), np.ones(16))
+    bad = fake(A)
+    bad.col_idx = bad.col_idx.clone()
+    bad.col_idx[2] += 1
+    assert StencilOperator.from_csr(bad) is None
+    bad = fake(A)
+    bad.row_ptr = bad.row_ptr.clone()
+    bad.row_ptr[3] -= 1
+    assert StencilOperator.from_csr(bad) is None
+    chain = types.SimpleNamespace(n=5, row_ptr=torch.tensor([0, 2, 5, 8, 11, 13]),
+                                  col_idx=torch.tensor([0, 1, 0, 1, 2, 1, 2, 3, 2, 3, 4, 3, 4], dtype=torch.int32),
+                                  values=torch.ones(13, dtype=torch.float64))
+    assert StencilOperator.from_csr(chain) is None
