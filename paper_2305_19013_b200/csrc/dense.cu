@@ -726,8 +726,11 @@ xr_update_kernel(const double* __restrict__ W, int ldw, const double* __restrict
 
 // m = 4*LN columns, 16-B aligned rows: LN lanes per row, 4 columns per lane,
 // U row groups in flight per warp (x and r loaded before the reductions).
+// 4 CTAs per SM: the fixed 1184-CTA grid (the partial count sets the summation order) is then exactly two
+// waves of 592 resident CTAs; at 3 per SM (78 registers) it ran 2.67 waves with an idle tail (3.00 -> 2.92 ms
+// at 4096^2 x 64, tools/kbench.py).
 template <int LN, int U, bool W256 = false>
-__global__ void __launch_bounds__(kVecThreads)
+__global__ void __launch_bounds__(kVecThreads, 4)
 xr_update4_kernel(const double* __restrict__ W, int ldw, const double* __restrict__ AW, int ldaw,
                   const double* __restrict__ alpha, double* __restrict__ x, double* __restrict__ r, long long n,
                   double* __restrict__ partials, const int* __restrict__ live) {
