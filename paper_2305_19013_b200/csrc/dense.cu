@@ -534,8 +534,7 @@ update_dmma_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
 }
 
 // Wide-block variant (M >= 32): the coefficient blocks C_i are staged once per
-// CTA in shared memory (rows padded to M + 4 doubles so the 4 k-rows of a
-// fragment fall 8 banks apart) and B fragments come from smem; 8 warps per
+// CTA in shared memory (rows padded to M + 2 doubles, see LDC below) and B fragments come from smem; 8 warps per
 // CTA, each walking its own 8*MR-row tiles (no block barriers in the loop).
 // TRI: d = 1 and C upper triangular (the Pre-CholQR / A-CholQR factor
 // S = R^-1, aortho.py:106,109): k-step pairs kp > nt multiply exact zeros and
@@ -549,7 +548,10 @@ update_smem_kernel(const double* const* __restrict__ Qs, int ldq, int d, const d
     extern __shared__ double cs[];
     constexpr int NT = M / 8;
     constexpr int KK = M / 4;
-    constexpr int LDC = M + 4;
+    // rows padded to M + 2 doubles: a B fragment reads k-rows 2 lr (+1), so consecutive lr are 2 rows = 4 bank
+    // pairs apart and the 16 lanes of a half warp (4 columns x 4 lr) hit 16 distinct bank pairs; with M + 4 the
+    // rows of lr and lr + 2 aliased (ncu: 51 % of the shared-load wavefronts were conflict replays)
+    constexpr int LDC = M + 2;
     // INIT: sign * C staged (exact for sign = +-1), so the accumulators start from beta * Win and the
     // tile is stored straight from them -- the Win loads issue with the first A fragments instead of
     // after the K loop, and no read-modify-write trails each tile (m = 64, d = 3: 29.9 -> 33.3 TFLOP/s).
@@ -978,8 +980,8 @@ extern "C" int ekcg_block_update(const double* const* Qs, int ldq, int d, int m1
     } else if (m1 == m2 && even && m1 == 16) {
         launch_k(update_dmma_kernel<16, 4, false>, grid_rows(32), 128, 0, st, Qs, ldq, d, C, Win, ldwi, Wout, ldwo, beta,
                                                                    sign, n, live);
-    } else if (m1 == m2 && even && (m1 == 32 || m1 == 64) && (size_t)d * m1 * (m1 + 4) * 8 <= 200 * 1024) {
-        const size_t smem = (size_t)d * m1 * (m1 + 4) * sizeof(double);
+    } else if (m1 == m2 && even && (m1 == 32 || m1 == 64) && (size_t)d * m1 * (m1 + 2) * 8 <= 200 * 1024) {
+        const size_t smem = (size_t)d * m1 * (m1 + 2) * sizeof(double);
         const int mr = (m1 == 32) ? 4 : EKCG_UPD64_MR;
         long long tiles = (n + 8 * mr - 1) / (8 * mr);
         unsigned grid = grid_for(tiles, 8, (long long)device_sms() * 8);
@@ -1013,7 +1015,7 @@ extern "C" int ekcg_tri_apply(const double* const* Ws, int ldw, const double* S,
     if (n == 0) return EKCG_OK;
     const bool even = (ldw % 2 == 0) && (ldo % 2 == 0) && (reinterpret_cast<uintptr_t>(out) % 16 == 0);
     if (m == 64 && even) {
-        const size_t smem = (size_t)64 * (64 + 4) * sizeof(double);
+        const size_t smem = (size_t)64 * (64 + 2) * sizeof(double);
         long long tiles = (n + 15) / 16;
         unsigned grid = grid_for(tiles, 8, (long long)device_sms() * 8);
         auto fn = update_smem_kernel<64, 2, true>;
