@@ -8,8 +8,9 @@ Fixtures (tests/golden/make_full_golden.py, generated in the build container):
   s-step method (solvers.py:59), so the fixture is the oracle's definition
   (bounded-memory restatement, bitwise run_oracle at small sizes);
 * full_cfg5.json -- the largest config-5 instance the bounded-memory oracle fits
-  in the build host's RAM (stated in the fixture; one full-size n x 64 block is
-  34.4 GB).
+  in the build host's RAM (4096^2, 8 iterations, 95 min; stated in the fixture;
+  one full-size n x 64 block is 34.4 GB); full_cfg5_2048.json -- 2048^2, 12
+  iterations.
 
 Each test rebuilds the inputs with the package's generators, checks them
 against the fixture's hashes (b, owner map, coefficient field), runs the device
@@ -112,6 +113,12 @@ def test_cfg4_full_size_vs_oracle():
 
 def test_cfg5_largest_oracle_instance():
     fx = _fixture("cfg5")
+    _run(5, fx)
+
+
+def test_cfg5_second_oracle_instance_2048():
+    """The first bounded-memory fixture (2048^2, 12 iterations: four more steady-state iterations than the 4096^2 one)."""
+    fx = _fixture("cfg5_2048")
     _run(5, fx)
 
 
