@@ -257,7 +257,8 @@ int ekcg_stencil_xr(const EkcgStencil* desc, const double* X, int ldx, double* Y
  * ekcg_start.  `blocks` is scratch of (2 window + 3) * span + n doubles (span >=
  * n t, a multiple of 32).  On return (stream order) ctrl holds the final
  * status / k_done / breakdown record, history[1..k_done] the residual norms,
- * checks[j] the true residual after iteration (j + 1) * every.  phase_ticks (may
+ * checks[j] the true residual after iteration (j + 1) * every.  A CSR matrix with a
+ * row of more than 8 entries is refused: ctrl->status = 5, nothing else written.  phase_ticks (may
  * be NULL) is a diagnostic: 20 device int64 that CTA 0 increments by the SM cycles
  * it spent in each phase of the iteration (tools/cluster_time.py names them). */
 int ekcg_cluster_solve_fits(long long n, int t, int window);
@@ -272,7 +273,8 @@ int ekcg_cluster_solve(const EkcgStencil* desc, const long long* row_ptr, const 
  * barrier and two scalar exchanges per iteration, no host reads inside the loop.  Before the
  * call: x = x0, r = b - A x0, ctrl / history[0] initialised by ekcg_start (tol_abs = tol * rho0).
  * `scratch` holds 2 n doubles (p, A p).  On return ctrl holds status (1 converged, 2 maxiter,
- * 3 = nonpositive curvature with brk_pivot = p^T A p and brk_iter = the iteration) and k_done. */
+ * 3 = nonpositive curvature with brk_pivot = p^T A p and brk_iter = the iteration, 5 = a CSR
+ * row of more than 8 entries: refused) and k_done. */
 int ekcg_cluster_cg(const EkcgStencil* desc, const long long* row_ptr, const int* col_idx,
                     const double* values, long long n, int kmax, double* x, double* r, double* scratch,
                     void* ctrl, double* history, void* stream);

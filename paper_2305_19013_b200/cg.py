@@ -98,6 +98,8 @@ def cg(A, b, x0=None, cfg=None, x_star=None, device=None):
         raw = ctrl.cpu().numpy()
         ints, dbl = raw[:32].view(np.int32), raw[32:80].view(np.float64)
         code, k_done = int(ints[1]), int(ints[2])
+        if code == 5:
+            raise _lib.KernelError("ekcg_cluster_cg refused the matrix: a CSR row holds more than 8 entries")
         history = list(hist[: k_done + 1].cpu().numpy())
         notes = []
         if code == 3:

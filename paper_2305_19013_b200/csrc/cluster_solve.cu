@@ -757,6 +757,15 @@ __device__ __forceinline__ int cholinv_local(Ctx& c, int m, double tol, int& col
     return res[0];
 }
 
+// CSR operators: true when no row of the matrix holds more than 8 entries (the operator rows keep 8 in
+// registers) -- agreed across the cluster, so every CTA takes the same branch.
+__device__ __forceinline__ bool rows_fit(Ctx& c, const Args& a, long long r0, long long r1) {
+    double bad = 0.0;
+    for (long long row = r0 + threadIdx.x; row < r1; row += kNT)
+        if (__ldg(a.rp + row + 1) - __ldg(a.rp + row) > 8) bad = 1.0;
+    return scalar_all(c, bad, R_ALPHA) == 0.0;  // a region no later exchange reuses before a cluster barrier
+}
+
 // M > 0: the block width is exactly M (compile-time index math); M == 0: runtime width a.t <= 8 MT.
 template <bool CSR, int MT, int M>
 __global__ void __launch_bounds__(kNT, 1) cluster_solve_kernel(const Args a) {
@@ -800,10 +809,17 @@ __global__ void __launch_bounds__(kNT, 1) cluster_solve_kernel(const Args a) {
 
     pdl_wait();
     EkcgCtrl* ctrl = a.ctrl;
-    const bool run = ctrl->live != 0;  // rho0 == 0: nothing to do (same value in every CTA)
+    bool run = ctrl->live != 0;  // rho0 == 0: nothing to do (same value in every CTA)
     const double tol_abs = ctrl->tol_abs;
     double best_rho = ctrl->best_rho;
     int best_k = ctrl->best_k;
+    if (CSR && run && !rows_fit(c, a, r0, r1)) {  // a row with more than 8 entries: refuse (status 5)
+        if (lead) {
+            ctrl->status = 5;
+            ctrl->live = 0;
+        }
+        run = false;
+    }
 
     double* WA = a.blocks + 2LL * win * a.span;
     double* WB = WA + a.span;
@@ -1066,8 +1082,15 @@ __global__ void __launch_bounds__(kNT, 1) cluster_cg_kernel(const CgArgs ca) {
 
     pdl_wait();
     EkcgCtrl* ctrl = a.ctrl;
-    const bool run = ctrl->live != 0;  // rho0 == 0: converged before the first iteration
+    bool run = ctrl->live != 0;  // rho0 == 0: converged before the first iteration
     const double tol_abs = ctrl->tol_abs;
+    if (CSR && run && !rows_fit(c, a, r0, r1)) {
+        if (lead) {
+            ctrl->status = 5;
+            ctrl->live = 0;
+        }
+        run = false;
+    }
     double* __restrict__ p = ca.p;
     double* __restrict__ ap = ca.ap;
     double rz = 0.0, rho = ctrl->last_rho, pAp = 0.0;

@@ -878,6 +878,8 @@ class DeviceEngine:
                   blocks.data_ptr(), span, self.ctrl.data_ptr(), self.history.data_ptr(), self.checks.data_ptr(),
                   1e-14, None if self.cluster_ticks is None else self.cluster_ticks.data_ptr(), self.stream)
         ctrl = self._read_ctrl()
+        if ctrl["status"] == 5:
+            raise _lib.KernelError("ekcg_cluster_solve refused the matrix: a CSR row holds more than 8 entries")
         self._cluster_blocks = blocks
         self.ran_cluster = True
         last = ctrl["k_done"] + (1 if ctrl["status"] == 3 else 0)

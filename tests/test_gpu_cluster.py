@@ -241,3 +241,44 @@ def test_cluster_cg_breakdown_and_kmax(monkeypatch):
     prob = make_config(1, 40)
     x, rep = pk.cg(prob.stencil(), prob.b, cfg=SolverConfig(method="cg", kmax=7))
     assert rep.status == "maxiter" and rep.iterations == 7 and len(rep.residual_history) == 8
+
+
+def test_cluster_kernels_refuse_rows_longer_than_8_entries():
+    """The C entry points check the CSR row lengths on the device (the Python dispatch never sends such a matrix)."""
+    import ctypes
+
+    from paper_2305_19013_b200 import _lib
+    n, t = 64, 2
+    dense = np.eye(n) * 20.0
+    for k in range(1, 6):  # 11 entries per interior row
+        dense += np.diag(np.full(n - k, -1.0), k) + np.diag(np.full(n - k, -1.0), -k)
+    r, c = np.nonzero(dense)
+    A = pk.SparseSpdMatrix.from_coo(n, r, c, dense[r, c])
+    op = pk.CsrOperator(A)
+    f64 = dict(dtype=torch.float64, device="cuda")
+    b = torch.ones(n, **f64)
+    x = torch.zeros(n, **f64)
+    rr = b.clone()
+    rho2 = (rr * rr).sum().reshape(1)
+    ctrl = torch.zeros(_lib.query("ekcg_ctrl_bytes"), dtype=torch.uint8, device="cuda")
+    hist = torch.zeros(50, **f64)
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.call("ekcg_start", ctrl.data_ptr(), rho2.data_ptr(), 1e-8, hist.data_ptr(), st)
+    owner = torch.arange(n, dtype=torch.int32, device="cuda") * t // n
+    blocks = torch.zeros(7 * 128 + 64, **f64)
+    checks = torch.zeros(50, **f64)
+    _lib.call("ekcg_cluster_solve", None, op.row_ptr.data_ptr(), op.col_idx.data_ptr(), op.values.data_ptr(), n, t, 2, 20,
+              50, owner.data_ptr(), b.data_ptr(), x.data_ptr(), rr.data_ptr(), blocks.data_ptr(), 128, ctrl.data_ptr(),
+              hist.data_ptr(), checks.data_ptr(), 1e-14, None, st)
+    assert int(ctrl.cpu().numpy()[:8].view(np.int32)[1]) == 5 and not torch.any(x)
+    _lib.call("ekcg_start", ctrl.data_ptr(), rho2.data_ptr(), 1e-8, hist.data_ptr(), st)
+    scratch = torch.zeros(2 * n, **f64)
+    _lib.call("ekcg_cluster_cg", None, op.row_ptr.data_ptr(), op.col_idx.data_ptr(), op.values.data_ptr(), n, 20,
+              x.data_ptr(), rr.data_ptr(), scratch.data_ptr(), ctrl.data_ptr(), hist.data_ptr(), st)
+    assert int(ctrl.cpu().numpy()[:8].view(np.int32)[1]) == 5 and not torch.any(x)
+    # the Python dispatch keeps such matrices on the launch-per-phase kernels
+    part = pk.Partition.from_owner(owner.cpu().numpy().astype(np.int64), t)
+    eng = DeviceEngine(A, part, SolverConfig(method="sre-cg2", t=t, retention="trunc", trunc=2, tol=1e-10))
+    xs, rep = eng.solve(np.ones(n))
+    assert not eng.ran_cluster and rep.status == "converged"
+    assert np.allclose(dense @ xs, np.ones(n), atol=1e-8)
