@@ -44,6 +44,11 @@ struct March {
     static_assert(ITEMS % NT == 0, "items per thread");
 };
 
+template <class P>
+__device__ __forceinline__ void march_apply(const double (&v)[7], unsigned mk, bool interior, const double* pm,
+                                            const double* pc, const double* pp, int ix, int iy, int ig,
+                                            double (&o)[4], int& ha, int& hb);
+
 // A X for one item: node (x0+ix, y0+iy) of plane w, columns 4 ig .. 4 ig+3 of
 // the chunk, from the staged planes pm / pc / pp (previous, current, next).
 // o[0..1] are columns 4 ig + ha (+1), o[2..3] columns 4 ig + hb (+1).
@@ -66,6 +71,16 @@ __device__ __forceinline__ void march_node(const EkcgStencil& s, const UniformFa
         mk = (DIM == 3) ? stencil_coef(s, uf, x, y, (unsigned)w, v)
                         : stencil_coef(s, uf, x, (unsigned)w, 0u, v);
     }
+    march_apply<P>(v, mk, interior, pm, pc, pp, ix, iy, ig, o, ha, hb);
+}
+
+// The products and sums of one item from its coefficient row v (slot order z-, y-, x-, diag, x+, y+, z+),
+// presence mask mk and the staged planes: p0 + (((p1 + p2) + ...)) over the present entries in order.
+template <class P>
+__device__ __forceinline__ void march_apply(const double (&v)[7], unsigned mk, bool interior, const double* pm,
+                                            const double* pc, const double* pp, int ix, int iy, int ig,
+                                            double (&o)[4], int& ha, int& hb) {
+    constexpr int DIM = P::DIM, KC = P::KC;
     const int hc = ((iy + P::OY) * P::PX + ix + 1) * KC + 4 * ig;
     // neighbour slices in entry order z-, y-, x-, diag, x+, y+, z+ (2-D: the march axis is y)
     const double* nb[7];
@@ -180,6 +195,60 @@ stencil_march_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil s, Un
         act[it] = (x0 + ix[it] < (int)nx) && (DIM == 2 || y0 + iy[it] < (int)ny) && (c0 + 4 * ig[it] + 4 <= m);
     }
 
+    // Tile fields with the host-built tables (kself, hx, hy, hz): the march axis (y in 2-D, z in 3-D) is shared
+    // by the whole CTA, so the tile layer and the position inside it are CTA-uniform -- a node's tile lookups
+    // and its in-plane faces are redone only when the march enters a new tile layer (a uniform branch), and a
+    // plane costs two selects for the march-axis faces and the diagonal's add chain instead of the full
+    // stencil_coef (tile divisions, 64-bit index math, face bookkeeping: ~60 % of this kernel's instructions
+    // were integer / control in ncu) or a 64-B table row per node.  Same IEEE operations in the same order as
+    // stencil_coef, so the same bits.
+    // (preferred over the per-node table when both are present: config 3 0.294 -> 0.246 ms; operators built
+    // from a CSR matrix have only the table)
+    const bool fastf = P::IPT == 1 && s.kfield != nullptr && s.kself != nullptr && s.hx != nullptr &&
+                       s.hy != nullptr && (DIM == 2 || s.hz != nullptr);
+    const int f_tw = (DIM == 3) ? s.tz : s.ty;           // tile edge along the march axis
+    const int f_sw = (DIM == 3) ? s.fx * s.fy : s.fx;    // field stride of one tile layer
+    int f_rw = 0, f_tc = 0;
+    double f_kc = 0.0, f_fwin = 0.0, f_fxl = 0.0, f_fxh = 0.0, f_fyl = 0.0, f_fyh = 0.0;
+    bool f_xlo = false, f_xhi = false, f_xlc = false, f_xhc = false;
+    bool f_ylo = false, f_yhi = false, f_ylc = false, f_yhc = false;
+    if (fastf) {
+        const unsigned x = (unsigned)(x0 + ix[0]);
+        const unsigned txi = tile_div(x, s.tx);
+        const unsigned rx = x - txi * (unsigned)s.tx;
+        f_xlo = x > 0;
+        f_xhi = x + 1 < nx;
+        f_xlc = rx == 0;
+        f_xhc = rx + 1 == (unsigned)s.tx;
+        unsigned tyi = 0;
+        if (DIM == 3) {
+            const unsigned y = (unsigned)(y0 + iy[0]);
+            tyi = tile_div(y, s.ty);
+            const unsigned ry = y - tyi * (unsigned)s.ty;
+            f_ylo = y > 0;
+            f_yhi = y + 1 < ny;
+            f_ylc = ry == 0;
+            f_yhc = ry + 1 == (unsigned)s.ty;
+        }
+        const unsigned twi = tile_div((unsigned)wb, f_tw);
+        f_rw = wb - (int)(twi * (unsigned)f_tw);
+        f_tc = (DIM == 3) ? ((int)twi * s.fy + (int)tyi) * s.fx + (int)txi : (int)twi * s.fx + (int)txi;
+    }
+    auto tile_layer = [&]() {  // the node's constants inside tile f_tc
+        f_kc = __ldg(s.kfield + f_tc);
+        const double ks = __ldg(s.kself + f_tc);
+        f_fwin = mul_rn(DIM == 3 ? s.cz : s.cy, ks);
+        const double fxin = mul_rn(s.cx, ks);
+        f_fxl = f_xlo ? (f_xlc ? __ldg(s.hx + f_tc - 1) : fxin) : 0.0;
+        f_fxh = f_xhi ? (f_xhc ? __ldg(s.hx + f_tc) : fxin) : 0.0;
+        if (DIM == 3) {
+            const double fyin = mul_rn(s.cy, ks);
+            f_fyl = f_ylo ? (f_ylc ? __ldg(s.hy + f_tc - s.fx) : fyin) : 0.0;
+            f_fyh = f_yhi ? (f_yhc ? __ldg(s.hy + f_tc) : fyin) : 0.0;
+        }
+    };
+    if (fastf && act[0]) tile_layer();
+
     for (int w = wb; w < we; ++w) {
         const int q = w - wb + 1;
         // one thread observes the TMA completions; the CTA barrier then both
@@ -206,11 +275,50 @@ stencil_march_kernel(const __grid_constant__ CUtensorMap tmap, EkcgStencil s, Un
             const unsigned x = x0 + ix[it], y = y0 + iy[it];
             double o[4];
             int ha, hb;
-            march_node<P>(s, uf, pm, pc, pp, x0, y0, ix[it], iy[it], ig[it], w, nx, ny, nw, o, ha, hb);
+            if (fastf) {
+                // march-axis faces: the tile-interior value, or the host-built cross-tile face on the layer's edges
+                const double* __restrict__ hw = (DIM == 3) ? s.hz : s.hy;
+                const double cw = (DIM == 3) ? s.cz : s.cy;
+                const bool wlo = w > 0, whi = (unsigned)w + 1 < nw;
+                const double fwh = whi ? (f_rw + 1 == f_tw ? __ldg(hw + f_tc) : f_fwin) : 0.0;
+                const double fwl = wlo ? (f_rw == 0 ? __ldg(hw + f_tc - f_sw) : f_fwin) : 0.0;
+                double diag = 0.0;  // the add order of stencil_coef: slowest axis first; +hi, +lo, +first, +last
+                if (whi) diag = add_rn(diag, fwh);
+                if (wlo) diag = add_rn(diag, fwl);
+                if (!wlo) diag = add_rn(diag, mul_rn(cw, f_kc));
+                if (!whi) diag = add_rn(diag, mul_rn(cw, f_kc));
+                if (DIM == 3) {
+                    if (f_yhi) diag = add_rn(diag, f_fyh);
+                    if (f_ylo) diag = add_rn(diag, f_fyl);
+                    if (!f_ylo) diag = add_rn(diag, mul_rn(s.cy, f_kc));
+                    if (!f_yhi) diag = add_rn(diag, mul_rn(s.cy, f_kc));
+                }
+                if (f_xhi) diag = add_rn(diag, f_fxh);
+                if (f_xlo) diag = add_rn(diag, f_fxl);
+                if (!f_xlo) diag = add_rn(diag, mul_rn(s.cx, f_kc));
+                if (!f_xhi) diag = add_rn(diag, mul_rn(s.cx, f_kc));
+                double v[7];
+                unsigned mk = (1u << 3) | (f_xlo ? 1u << 2 : 0u) | (f_xhi ? 1u << 4 : 0u);
+                if (DIM == 3) {
+                    v[0] = -fwl; v[1] = -f_fyl; v[2] = -f_fxl; v[3] = diag; v[4] = -f_fxh; v[5] = -f_fyh; v[6] = -fwh;
+                    mk |= (wlo ? 1u : 0u) | (f_ylo ? 1u << 1 : 0u) | (f_yhi ? 1u << 5 : 0u) | (whi ? 1u << 6 : 0u);
+                } else {
+                    v[0] = 0.0; v[1] = -fwl; v[2] = -f_fxl; v[3] = diag; v[4] = -f_fxh; v[5] = -fwh; v[6] = 0.0;
+                    mk |= (wlo ? 1u << 1 : 0u) | (whi ? 1u << 5 : 0u);
+                }
+                march_apply<P>(v, mk, mk == ((DIM == 3) ? 0x7fu : 0x3eu), pm, pc, pp, ix[it], iy[it], ig[it], o, ha, hb);
+            } else {
+                march_node<P>(s, uf, pm, pc, pp, x0, y0, ix[it], iy[it], ig[it], w, nx, ny, nw, o, ha, hb);
+            }
             const long long row = (DIM == 3) ? ((long long)w * ny + y) * nx + x : (long long)w * nx + x;
             double* yr = Y + row * ldy + c0 + 4 * ig[it];
             *reinterpret_cast<double2*>(yr + ha) = make_double2(o[0], o[1]);
             *reinterpret_cast<double2*>(yr + hb) = make_double2(o[2], o[3]);
+        }
+        if (fastf && ++f_rw == f_tw) {  // the next plane starts a new tile layer (CTA-uniform)
+            f_rw = 0;
+            f_tc += f_sw;
+            if (w + 1 < we && act[0]) tile_layer();
         }
     }
 }
