@@ -32,6 +32,7 @@ CASES = {
     "r02_cfg5full_hist_update": ("5 (8192^2, lean)", "hist_update", N5, 64, 3, 0, 0),
     "r02_cfg5full_stencil": ("5 (8192^2)", "stencil", N5, 64, 0, 5 * N5 - 4 * 8192, 512 * 512 * 8),
     "r02_cfg5full_stencil_waves": ("5 (8192^2), whole-wave chunks", "stencil", N5, 64, 0, 5 * N5 - 4 * 8192, 512 * 512 * 8),
+    "r02_cfg5full_stencil_hoisted": ("5 (8192^2), + tile-layer hoisting", "stencil", N5, 64, 0, 5 * N5 - 4 * 8192, 512 * 512 * 8),
     "r02_cfg5full_hist_gram": ("5 (8192^2, lean)", "hist_gram", N5, 64, 3, 0, 0),
     "r02_cfg5full_tri_apply": ("5 (8192^2, lean)", "tri_apply", N5, 64, 0, 0, 0),
     "r02_cfg5_hist_gram": ("5 (4096^2)", "hist_gram", N5Q, 64, 3, 0, 0),
@@ -40,6 +41,7 @@ CASES = {
     "r02_cfg3_hist_gram": ("3 (128^3)", "hist_gram", N3, 32, 4, 0, 0),
     "r02_cfg3_stencil": ("3 (128^3)", "stencil", N3, 32, 0, 7 * N3 - 6 * 128 ** 2, 8 * N3),
     "r02_cfg3_stencil_waves": ("3 (128^3), whole-wave chunks", "stencil", N3, 32, 0, 7 * N3 - 6 * 128 ** 2, 8 * N3),
+    "r02_cfg3_stencil_hoisted": ("3 (128^3), + tile-layer hoisting", "stencil", N3, 32, 0, 7 * N3 - 6 * 128 ** 2, 8 * N3),
     "r02_cfg4_hist_update": ("4 (256^3)", "hist_update", N4, 64, 2, 0, 0),
     "r02_cfg4_hist_gram": ("4 (256^3)", "hist_gram", N4, 64, 2, 0, 0),
     "r02_cfg4_stencil": ("4 (256^3)", "stencil", N4, 64, 0, 7 * N4 - 6 * 256 ** 2, 0),
