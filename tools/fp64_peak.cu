@@ -40,6 +40,19 @@ int main(){
     cudaEventElapsedTime(&ms,e0,e1);
     fl=2.0*256*8*(iters/4)*(double)grid*(thr/32); printf("DMMA bps=%d: %.2f TFLOP/s\n",blocks_per_sm, fl/ms/1e9);
   }
+  {  // sustained DMMA rate: back-to-back launches for ~4 s, rate over the last 2 s (the power-capped clock;
+     // the denominator for a kernel timed inside a long step, like MEASURED_PEAKS.json's bf16_tflops_sustained)
+    int grid=sms*8, thr=256, iters=20000;
+    double per_launch=2.0*256*8*iters*(double)grid*(thr/32);
+    cudaEvent_t t0,t1; cudaEventCreate(&t0); cudaEventCreate(&t1);
+    float total=0; int launches=0; double last_fl=0; float last_ms=0;
+    while(total<4000.f){
+      cudaEventRecord(t0); for(int r=0;r<10;r++) dmma_k<<<grid,thr>>>(out,iters); cudaEventRecord(t1); CK(cudaEventSynchronize(t1));
+      float ms; cudaEventElapsedTime(&ms,t0,t1); total+=ms; launches+=10;
+      if(total>2000.f){ last_fl+=10*per_launch; last_ms+=ms; }
+    }
+    printf("DMMA sustained (last %.0f ms of %.0f ms, %d launches): %.2f TFLOP/s\n", last_ms, total, launches, last_fl/last_ms/1e9);
+  }
   size_t n=(size_t)1<<28; double2 *a,*b; CK(cudaMalloc(&a,n*16)); CK(cudaMalloc(&b,n*16));
   cudaMemset(a,0,n*16);
   for(int g: {sms*2, sms*4, sms*8}){
