@@ -74,11 +74,17 @@ def main():
             ms = e0.elapsed_time(e1)
             by[tag][0] += ms
             by[tag][1] += 1
+    by_d = defaultdict(lambda: [0.0, 0])  # the CGS2 kernels per history depth d
+    for tag, cur, e0, e1 in hook.used:
+        if cur[0] <= rep_.iterations and tag in ("hist_gram", "hist_update"):
+            by_d[f"{tag}@d={cur[1]}"][0] += e0.elapsed_time(e1)
+            by_d[f"{tag}@d={cur[1]}"][1] += 1
     tagged = sum(v[0] for v in by.values())
     out = {"config": prob.name, "iterations": rep_.iterations, "total_ms": round(total, 2),
            "ms_per_it": round(total / max(rep_.iterations, 1), 4),
            "tags": {k: {"ms": round(v[0], 2), "n": v[1], "share": round(v[0] / total, 3)}
                     for k, v in sorted(by.items(), key=lambda kv: -kv[1][0])},
+           "cgs2_ms_per_launch_by_depth": {k: round(v[0] / v[1], 3) for k, v in sorted(by_d.items())},
            "untagged_share": round(1 - tagged / total, 3),
            "model_GBs": rep_.model_bytes / (total / 1e3) / 1e9}
     print(json.dumps(out), flush=True)
