@@ -13,7 +13,9 @@ _lib._LIB_PATH = Path(sys.argv[1]).resolve()
 from paper_2305_19013_b200.problems import make_config  # noqa: E402
 
 st = torch.cuda.current_stream().cuda_stream
-for idx, edge, m in ((5, 8192, 64), (3, 128, 32)):
+CASES = ((5, 8192, 64), (3, 128, 32), (4, 256, 64), (4, 256, 16), (2, 64, 16)) if "--all" in sys.argv else \
+    ((5, 8192, 64), (3, 128, 32))
+for idx, edge, m in CASES:
     prob = make_config(idx, edge, device_rhs=False)
     op = prob.stencil("cuda")
     g = torch.Generator(device="cuda").manual_seed(3)
