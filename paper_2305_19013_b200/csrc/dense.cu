@@ -90,6 +90,77 @@ __device__ __forceinline__ void load_tiles(const double* row, int lc, bool ok, d
 }
 
 // ---------------------------------------------------------------------------
+// X^T X for one 64-column block (the Pre-CholQR Gram W^T W, aortho.py:105) over rows [r0, r1): a tile below
+// the diagonal is the transpose of its mirror above it -- same products, same order, same bits -- so only
+// the 36 of 64 8 x 8 tiles on and above the diagonal are formed and each is stored twice.  Warps 0 / 3 take
+// the diagonal 32 x 32 quadrants (10 tiles each; the B fragments are the A fragments), warps 1 / 2 the left
+// and right halves of the quadrant above the diagonal (8 tiles each).  Kept out of line so that the general
+// kernel's registers and schedule stay as they are.
+// ---------------------------------------------------------------------------
+template <int U>
+__device__ __noinline__ void gram_self64(const double* __restrict__ Y, int ldy, long long r0, long long r1,
+                                         double* __restrict__ out) {
+    constexpr int M = 64, T = 4;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lr = lane & 3, lc = lane >> 2;
+    const long long steps = (r1 > r0) ? (r1 - r0 + 3) / 4 : 0;
+    const bool diag = warp == 0 || warp == 3;
+    const int a_off = warp == 3 ? 32 : 0;
+    const int b_off = warp == 0 ? 0 : warp == 2 ? 48 : 32;
+    double acc[T][T][2];
+#pragma unroll
+    for (int ta = 0; ta < T; ++ta)
+#pragma unroll
+        for (int tb = 0; tb < T; ++tb) acc[ta][tb][0] = acc[ta][tb][1] = 0.0;
+    if (diag) {
+        for (long long s0 = 0; s0 < steps; s0 += U) {
+            double af[U][T];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long r = r0 + 4 * (s0 + u) + lr;
+                load_tiles<T, false>(Y + r * ldy + a_off, lc, r < r1, af[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int ta = 0; ta < T; ++ta)
+#pragma unroll
+                    for (int tb = ta; tb < T; ++tb) dmma_8x8x4(acc[ta][tb], af[u][ta], af[u][tb]);
+        }
+    } else {
+        for (long long s0 = 0; s0 < steps; s0 += U) {
+            double af[U][T], bf[U][2];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const long long r = r0 + 4 * (s0 + u) + lr;
+                load_tiles<2, false>(Y + r * ldy + b_off, lc, r < r1, bf[u]);
+                load_tiles<T, false>(Y + r * ldy + a_off, lc, r < r1, af[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int ta = 0; ta < T; ++ta)
+#pragma unroll
+                    for (int tb = 0; tb < 2; ++tb) dmma_8x8x4(acc[ta][tb], af[u][ta], bf[u][tb]);
+        }
+    }
+#pragma unroll
+    for (int ta = 0; ta < T; ++ta)
+#pragma unroll
+        for (int tb = 0; tb < T; ++tb) {
+            if (diag ? tb < ta : tb >= 2) continue;
+            const int a = a_off + 8 * ta + lc;
+            const int b0 = b_off + 8 * tb + 2 * lr, b1 = b0 + 1;
+            out[a * M + b0] = acc[ta][tb][0];
+            out[a * M + b1] = acc[ta][tb][1];
+            if (!(diag && ta == tb)) {
+                out[b0 * M + a] = acc[ta][tb][0];
+                out[b1 * M + a] = acc[ta][tb][1];
+            }
+        }
+}
+
+// ---------------------------------------------------------------------------
 // DMMA Gram: partials[p][i] (M x M) = X_i[rows of p]^T Y[rows of p]
 // CTA (p, g) handles row chunk p for blocks i = g*GB .. g*GB+GB-1, so each Y
 // fragment loaded feeds GB blocks.  Warp w: row lane ks = w % KS, output
@@ -134,13 +205,11 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
 
     const int lr = lane & 3;
     const int lc = lane >> 2;
-    // X^T X (the Pre-CholQR Gram W^T W, aortho.py:105): the quadrant below the
-    // diagonal is the transpose of the one above it -- same products, same
-    // order -- so its warp skips the DMMAs and the mirror warp stores both.
-    constexpr int QB = M / 8 / TB;
-    const bool sym = QA == 2 && QB == 2 && KS == 1 && GB == 1 && d == 1 && X[0] == Y;
-    const int qa = quad % QA, qb = quad / QA;
-    if (sym && qa > qb) return;  // no block barrier follows when KS == 1
+    // X^T X at m = 64 (plain 8-column tiles): only the tiles on and above the diagonal (gram_self64)
+    if (M == 64 && TA == 4 && TB == 4 && KS == 1 && GB == 1 && !IL && d == 1 && X[0] == Y) {
+        gram_self64<U>(Y, ldy, r0, r1, partials + (long long)blockIdx.y * (M * M));
+        return;
+    }
     for (long long s0 = ks; s0 < steps; s0 += (long long)KS * U) {
         double af[U][GB][TA], bf[U][TB];
 #pragma unroll
@@ -175,10 +244,6 @@ gram_dmma_kernel(const double* const* __restrict__ Xs, int ldx, int d, const dou
                     const int b0 = b_base + tile_col<TB, IL>(tb, 2 * lr), b1 = b_base + tile_col<TB, IL>(tb, 2 * lr + 1);
                     out[a * M + b0] = acc[g][ta][tb][0];
                     out[a * M + b1] = acc[g][ta][tb][1];
-                    if (sym && qa < qb) {
-                        out[b0 * M + a] = acc[g][ta][tb][0];
-                        out[b1 * M + a] = acc[g][ta][tb][1];
-                    }
                 }
         }
     } else {
