@@ -247,8 +247,8 @@ def tag_model(tag, n, m, d, nnz, mat_bytes):
         return 8.0 * (d + 1) * nm, 2.0 * d * m * nm
     if tag == "hist_update":    # W - sum Q_i C_i
         return 8.0 * (d + 2) * nm, 2.0 * d * m * nm
-    if tag == "gram_self":      # W^T W (one block read)
-        return 8.0 * nm, 2.0 * m * nm
+    if tag == "gram_self":      # W^T W (one block read; symmetric: m (m + 1) / 2 distinct entries)
+        return 8.0 * nm, (m + 1.0) * nm
     if tag == "gram_aw":        # W0^T (A W0)
         return 16.0 * nm, 2.0 * m * nm
     if tag in ("spmm", "spmm_proj", "spmm_chain"):
