@@ -23,6 +23,9 @@ def test_tag_model_matches_design(bench):
     assert bench.tag_model("hist_gram", n, m, d, 0, 0) == (8.0 * (d + 1) * nm, 2.0 * d * m * nm)
     assert bench.tag_model("hist_update", n, m, d, 0, 0) == (8.0 * (d + 2) * nm, 2.0 * d * m * nm)
     assert bench.tag_model("tri_apply", n, m, 0, 0, 0) == (16.0 * nm, 1.0 * m * nm)
+    # W^T W is symmetric: m (m + 1) / 2 distinct entries of 2 n flops each, one block read
+    assert bench.tag_model("gram_self", n, m, 0, 0, 0) == (8.0 * nm, (m + 1.0) * nm)
+    assert bench.tag_model("gram_aw", n, m, 0, 0, 0) == (16.0 * nm, 2.0 * m * nm)
     assert bench.tag_model("spmm", n, m, 0, 5 * n, 8 * n) == (16.0 * nm + 8 * n, 2.0 * 5 * n * m)
     assert bench.tag_model("unknown", n, m, 0, 0, 0) is None
 
