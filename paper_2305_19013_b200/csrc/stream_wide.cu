@@ -41,6 +41,89 @@ struct GramWide {
     static_assert(M % 16 == 0, "pairs of interleaved 8-wide tiles");
 };
 
+// ---------------------------------------------------------------------------
+// W^T W for one 32-column block (the Pre-CholQR Gram, aortho.py:105) on the
+// same ring: the block is streamed once and read as both operands, and only
+// the 10 of 16 8 x 8 tiles on and above the diagonal are formed -- a tile
+// below it is the transpose of its mirror (same products, same order, same
+// bits), so each tile is stored twice.  Out of line, so the general kernel's
+// registers and schedule stay as they are.
+// ---------------------------------------------------------------------------
+template <int R, int NS>
+__device__ __noinline__ void gram32_self(const double* __restrict__ Y, long long r0, long long r1, int nsteps,
+                                         double* sm, unsigned long long* full, unsigned long long* empty,
+                                         double* __restrict__ out) {
+    constexpr int M = 32, T = 4, H = 2, SLAB = R * M;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 4) {  // producer: one slab per stage
+        if (lane == 0) {
+            for (int j = 0; j < nsteps; ++j) {
+                const int slot = j % NS;
+                if (j >= NS) {
+                    mbar_wait(&empty[slot], ((j / NS) - 1) & 1);
+                    fence_proxy_async_smem();
+                }
+                const long long rb = r0 + (long long)j * R;
+                const unsigned bytes = (unsigned)(min((long long)R, r1 - rb) * M * sizeof(double));
+                mbar_expect_tx(&full[slot], bytes);
+                bulk_load(sm + slot * SLAB, Y + rb * M, bytes, &full[slot]);
+            }
+        }
+        return;
+    }
+    const int lr = lane & 3, lc = lane >> 2;
+    double acc[T][T][2];
+#pragma unroll
+    for (int a = 0; a < T; ++a)
+#pragma unroll
+        for (int b = 0; b < T; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    for (int j = 0; j < nsteps; ++j) {
+        const int slot = j % NS;
+        mbar_wait(&full[slot], (j / NS) & 1);
+        const double* st = sm + slot * SLAB;
+        const int rr = (int)min((long long)R, r1 - (r0 + (long long)j * R));
+#pragma unroll
+        for (int q = 0; q < R / 16; ++q) {
+            const int row = (q * 4 + warp) * 4 + lr;
+            const bool ok = row < rr;
+            double f[T];
+#pragma unroll
+            for (int h = 0; h < H; ++h) {
+                const double2 v = ok ? *reinterpret_cast<const double2*>(st + row * M + 16 * h + 2 * lc) : make_double2(0.0, 0.0);
+                f[2 * h] = v.x;
+                f[2 * h + 1] = v.y;
+            }
+#pragma unroll
+            for (int a = 0; a < T; ++a)
+#pragma unroll
+                for (int b = a; b < T; ++b) dmma_8x8x4(acc[a][b], f[a], f[b]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    // fixed-order reduction of the four consumer warps' accumulators (as in the general kernel)
+    named_sync(1, 128);
+    double* red = sm;
+#pragma unroll
+    for (int ta = 0; ta < T; ++ta)
+#pragma unroll
+        for (int tb = ta; tb < T; ++tb)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int a = 16 * (ta / 2) + 2 * lc + (ta % 2);
+                const int b = 16 * (tb / 2) + 2 * (2 * lr + e) + (tb % 2);
+                red[(warp * M + a) * M + b] = acc[ta][tb][e];
+                if (tb > ta) red[(warp * M + b) * M + a] = acc[ta][tb][e];
+            }
+    named_sync(1, 128);
+    for (int o = threadIdx.x; o < M * M; o += 128) {
+        double v = red[o];
+#pragma unroll
+        for (int w = 1; w < 4; ++w) v += red[w * M * M + o];
+        out[o] = v;
+    }
+}
+
 template <int M, int GB, int R, int NS>
 __global__ void __launch_bounds__(160)
 gram_wide_stream_kernel(const double* const* __restrict__ Xs, int d, const double* __restrict__ Y, long long n,
@@ -66,6 +149,10 @@ gram_wide_stream_kernel(const double* const* __restrict__ Xs, int d, const doubl
     }
     __syncthreads();
 
+    if (M == 32 && GB == 1 && d == 1 && Xs[0] == Y) {  // W^T W: tiles on and above the diagonal, one stream
+        gram32_self<R, NS>(Y, r0, r1, nsteps, sm, full, empty, partials + (long long)blockIdx.x * (M * M));
+        return;
+    }
     if (warp == 4) {  // producer
         if (lane == 0) {
             const double* X[GB];

@@ -283,11 +283,11 @@ def test_vec256_paths_bitwise(m):
     assert np.max(np.abs(outs[1][0] - ref)) <= 1e-12 * np.max(np.abs(ref))
 
 @pytest.mark.parametrize("n", [37, 4099, 200_000])
-@pytest.mark.parametrize("m", [16, 64])
+@pytest.mark.parametrize("m", [16, 32, 64])
 def test_gram_self_symmetric_shortcut(n, m):
-    """X^T X (the Pre-CholQR Gram): at m = 64 the quadrant below the diagonal mirrors
-    the one above, at m = 16 the block is streamed once and read as both operands;
-    bitwise equal to X^T Y with Y a copy of X."""
+    """X^T X (the Pre-CholQR Gram): at m = 32 / 64 only the 8 x 8 tiles on and above the
+    diagonal are formed and each is stored with its mirror, at m = 16 / 32 the block is
+    streamed once and read as both operands; bitwise equal to X^T Y with Y a copy of X."""
     X = dev(np.random.default_rng(n).standard_normal((n, m)))
     Xc = X.clone()
     tab = torch.tensor([X.data_ptr()], dtype=torch.int64, device=DEV)
