@@ -296,7 +296,10 @@ class KernelTimer:
         e0.record()
         fn()
         e1.record()
-        self.used.append((tag,) + tuple(cur))
+        k, d, m = cur
+        if tag == "spmm_chain":  # the s-step chain applies A to one t-column slab of the s t-wide block
+            m //= max(1, int(getattr(self.engine, "s", 1)))
+        self.used.append((tag, k, d, m))
 
     def harvest(self, k_done):
         """Call after a full device sync; drops launches past the stopping iteration."""
